@@ -1,0 +1,195 @@
+/*
+ * include/fmm.h — C ABI of the B200-native 3D Laplace FMM mat-vec (libfmm.so).
+ *
+ * The operation (arXiv:1602.02244, Yokota/Ibeid/Keyes):
+ *   phi_i = sum_{j : |x_i - x_j| > 0} q_j / |x_i - x_j|          (kernel 1/r, no 4*pi)
+ *   grad_i = grad_{x_i} phi(x_i) = - sum_j q_j (x_i - x_j) / |x_i - x_j|^3
+ * evaluated as the analytic, matrix-free H^2 mat-vec of the fast multipole
+ * method: "a matrix-free H^2-matrix-vector product" (§1), whose
+ * far field is "approximated with multipole/local expansions" over a
+ * "hierarchically decomposed" domain, with interaction lists
+ * from a "dual tree traversal along with the multipole acceptance criterion"
+ * (§2.2). The direct operator (P2P) is the dense diagonal
+ * block, the translation operators the off-diagonal blocks.
+ * The paper times "the compression/precalculation and application of the
+ * matrix-vector multiplication" separately (§4.1): hence the
+ * split fmm_setup (precalculation: tree + lists) / fmm_matvec (application).
+ * It asks for "a common interface between the hierarchical structure and
+ * inner kernels" (§5): this header is that interface.
+ *
+ * Readings the paper leaves open (after SURVEY §8(c)):
+ *   - "order p" = solid-harmonic degrees 0..p ((p+1)^2 real coefficients);
+ *   - adaptive octree on 63-bit Morton keys (21 bits/axis), a cell splits iff
+ *     it holds more than ncrit points and its level is < 21;
+ *   - MAC: a cell pair (A,B) is translated by M2L iff theta^2 * D^2 > (H_A+H_B)^2,
+ *     D = distance of the cell centres, H = half side (integer-exact), valid
+ *     theta in (0, 1/sqrt(3)); split the larger cell, target on ties.
+ *
+ * Conventions for every call:
+ *   - All array pointers are DEVICE pointers on ex->device unless the name ends
+ *     in _host. Coordinates are [n][3] row-major doubles, charges / potentials
+ *     [n] doubles, gradients [n][3] row-major doubles, all fp64, caller order.
+ *   - The caller owns every buffer it passes; no caller pointer is retained
+ *     after a call returns. The plan owns all internal device memory.
+ *   - Work is enqueued on ex->stream (a cudaStream_t; NULL = legacy default).
+ *     fmm_setup synchronises that stream (list sizes are data dependent);
+ *     fmm_matvec and fmm_direct are stream ordered and return after enqueue
+ *     (the caller synchronises before reading results); fmm_matvec_host is
+ *     synchronous.
+ *   - Results are in the caller's input order and are bitwise deterministic for
+ *     identical inputs on the same device (no floating-point atomics).
+ *   - Calls on one plan must be serialised. Tree, lists and tables are immutable
+ *     after setup; expansion scratch is reused by every matvec.
+ *   - Errors: every call returns an fmm_status; the library never aborts or
+ *     exits. fmm_last_error() returns a thread-local message for the last
+ *     non-OK status. After any status other than FMM_OK / FMM_ERR_USAGE /
+ *     FMM_ERR_NUMERIC the plan is poisoned and only fmm_destroy is valid.
+ */
+#ifndef FMM_H
+#define FMM_H
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FMM_API __attribute__((visibility("default")))
+#else
+#define FMM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FMM_OK = 0,
+  FMM_ERR_USAGE = 2,   /* bad argument: sizes, ranges, NULL, non-finite coordinate */
+  FMM_ERR_NUMERIC = 3, /* non-finite charge or result */
+  FMM_ERR_CUDA = 4,    /* CUDA launch / runtime error (plan poisoned) */
+  FMM_ERR_OOM = 5,     /* device or host allocation failure (plan poisoned) */
+  FMM_ERR_COMM = 6     /* multi-GPU exchange error (plan poisoned) */
+} fmm_status;
+
+typedef struct fmm_plan_s* fmm_plan; /* opaque */
+
+/* Execution context. */
+typedef struct {
+  int device;     /* CUDA ordinal this process drives */
+  void* stream;   /* cudaStream_t; NULL = legacy default stream */
+  int rank;       /* 0 .. world_size-1 (multi-GPU: one process per GPU) */
+  int world_size; /* 1 = single GPU. For world_size > 1 every rank passes the
+                     GLOBAL point set to fmm_setup (the Python layer all-gathers
+                     caller slices over NCCL) and fmm_matvec evaluates only the
+                     targets of this rank's Morton range, see fmm_matvec. */
+} fmm_exec;
+
+/* Filled by fmm_stats. Times are CUDA-event milliseconds of the last call. */
+enum {
+  FMM_T_SORT = 0, FMM_T_TREE = 1, FMM_T_TRAVERSE = 2, FMM_T_SETUP_TOTAL = 3,
+  FMM_T_UPWARD = 0, FMM_T_M2L = 1, FMM_T_NEAR = 2, FMM_T_DOWNWARD = 3, FMM_T_MATVEC_TOTAL = 4
+};
+typedef struct {
+  int64_t n, n_cells, n_leaves, n_p2p_pairs, n_m2l_pairs, n_p2p_interactions;
+  int64_t own_begin, own_end; /* this rank's target range in Morton order */
+  int32_t p, ncrit, max_level, exponent; /* exponent e of the exact 2^-e normalisation */
+  double theta;
+  double t_setup_ms[8];  /* FMM_T_SORT .. FMM_T_SETUP_TOTAL */
+  double t_matvec_ms[8]; /* FMM_T_UPWARD .. FMM_T_MATVEC_TOTAL (0 unless timing enabled) */
+  int64_t bytes_device;  /* device memory owned by the plan */
+} fmm_stats_t;
+
+/*
+ * fmm_setup — precalculation: bounding cube, Morton keys,
+ * device radix sort, adaptive octree, dual tree traversal -> P2P and M2L lists.
+ *   out   : receives the new plan (NULL on error)
+ *   xyz   : device [n][3] fp64 point coordinates (copied; may be freed after return)
+ *   n     : number of points, >= 1 (global count when world_size > 1)
+ *   p     : expansion order, 0 <= p <= 16
+ *   ncrit : maximum leaf population, >= 1
+ *   theta : MAC parameter, 0 < theta < 1/sqrt(3)
+ *   ex    : execution context (non-NULL)
+ * Errors: FMM_ERR_USAGE for any argument outside the ranges above or a
+ * non-finite coordinate; FMM_ERR_OOM; FMM_ERR_CUDA.
+ */
+FMM_API fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncrit, double theta,
+                     const fmm_exec* ex);
+
+/*
+ * fmm_matvec — application: phi (+ grad) for charges q, on ex->stream.
+ *   q    : device [n] fp64 charges, caller order
+ *   n    : must equal the setup n (FMM_ERR_USAGE otherwise)
+ *   phi  : device [n] fp64 output, caller order
+ *   grad : device [n][3] fp64 output or NULL
+ * With world_size > 1 only the entries of targets owned by this rank (Morton
+ * range [own_begin, own_end) of fmm_stats) are written; the others are set to 0,
+ * so a sum over ranks (reduce-scatter) assembles the global result exactly.
+ * Non-finite charges give FMM_ERR_NUMERIC, detected on the device and reported
+ * by the NEXT fmm_matvec / fmm_sync call on the plan (the call is stream ordered).
+ */
+FMM_API fmm_status fmm_matvec(fmm_plan plan, const double* q, int64_t n, double* phi, double* grad);
+
+/*
+ * fmm_matvec_host — the same with HOST buffers (pinned or pageable): copies q
+ * host->device, runs fmm_matvec, copies phi (+grad) device->host, synchronises.
+ * This is the end-to-end entry point a host application calls.
+ */
+FMM_API fmm_status fmm_matvec_host(fmm_plan plan, const double* q_host, int64_t n, double* phi_host,
+                           double* grad_host);
+
+/* fmm_sync — synchronise the plan's stream and report deferred device errors. */
+FMM_API fmm_status fmm_sync(fmm_plan plan);
+
+/*
+ * fmm_direct — O(n_src * n_tgt) direct sum for checking (north_star):
+ *   phi_t = sum_{s : r > 0} q_s / r_ts, grad_t = -sum_s q_s (x_t - x_s) / r_ts^3.
+ * All pointers device, [n][3] / [n] fp64; grad may be NULL; n_src, n_tgt >= 0.
+ * Stream ordered on ex->stream.
+ */
+FMM_API fmm_status fmm_direct(const double* src_xyz, const double* q, int64_t n_src, const double* tgt_xyz,
+                      int64_t n_tgt, double* phi, double* grad, const fmm_exec* ex);
+
+/* fmm_stats — counts and timings of the plan (host struct). */
+FMM_API fmm_status fmm_stats(fmm_plan plan, fmm_stats_t* out);
+
+/* fmm_set_timing — enable (1) / disable (0) per-stage CUDA-event timing in fmm_matvec. */
+FMM_API fmm_status fmm_set_timing(fmm_plan plan, int enable);
+
+/*
+ * fmm_export — copy an internal array of the plan to a HOST buffer, for stage
+ * tests against the oracle. `what` selects the array; `capacity` is the size of
+ * `dst` in elements; *count receives the element count (call with dst = NULL to
+ * query it). Arrays (element type):
+ *   FMM_X_KEYS     uint64  [n]          sorted Morton keys
+ *   FMM_X_PERM     uint32  [n]          sorted position -> input index
+ *   FMM_X_LEVEL    int32   [ncells]     cells in breadth-first (level, Morton) order
+ *   FMM_X_ANCHOR   int32   [ncells][3]
+ *   FMM_X_BEGIN    int32   [ncells]     particle range [begin, end) in sorted order
+ *   FMM_X_END      int32   [ncells]
+ *   FMM_X_CHILD    int32   [ncells]     first child, -1 for a leaf
+ *   FMM_X_NCHILD   int32   [ncells]
+ *   FMM_X_PARENT   int32   [ncells]     -1 for the root
+ *   FMM_X_CENTER   double  [ncells][3]  centres in the 2^-e normalised frame
+ *   FMM_X_P2P      int32   [n_p2p][2]   (target leaf, source leaf), grouped by target
+ *   FMM_X_M2L      int32   [n_m2l][2]   (target cell, source cell), grouped by target
+ *   FMM_X_M        double  [ncells][(p+1)(p+2)/2][2]  multipoles of the last matvec
+ *   FMM_X_L        double  [ncells][(p+1)(p+2)/2][2]  local expansions of the last matvec
+ *   FMM_X_GEOM     double  [5]          lo_x, lo_y, lo_z, S, scale (normalised frame)
+ * Expansions: complex coefficients for m >= 0, index n(n+1)/2 + m, normalised frame.
+ */
+typedef enum {
+  FMM_X_KEYS = 0, FMM_X_PERM, FMM_X_LEVEL, FMM_X_ANCHOR, FMM_X_BEGIN, FMM_X_END, FMM_X_CHILD,
+  FMM_X_NCHILD, FMM_X_PARENT, FMM_X_CENTER, FMM_X_P2P, FMM_X_M2L, FMM_X_M, FMM_X_L, FMM_X_GEOM
+} fmm_array;
+FMM_API fmm_status fmm_export(fmm_plan plan, int what, void* dst, int64_t capacity, int64_t* count);
+
+/* fmm_destroy — free the plan (NULL is a no-op). */
+FMM_API void fmm_destroy(fmm_plan plan);
+
+/* fmm_last_error — thread-local message for the last non-OK status ("" if none). */
+FMM_API const char* fmm_last_error(void);
+
+/* fmm_version — library version string. */
+FMM_API const char* fmm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMM_H */

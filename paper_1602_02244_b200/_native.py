@@ -1,0 +1,76 @@
+"""ctypes declarations for libfmm.so (include/fmm.h). Argument marshalling only.
+
+The CUDA library is mandatory: importing this module raises if libfmm.so is
+missing or cannot be loaded. There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfmm.so")
+
+FMM_OK, FMM_ERR_USAGE, FMM_ERR_NUMERIC, FMM_ERR_CUDA, FMM_ERR_OOM, FMM_ERR_COMM = 0, 2, 3, 4, 5, 6
+
+(FMM_X_KEYS, FMM_X_PERM, FMM_X_LEVEL, FMM_X_ANCHOR, FMM_X_BEGIN, FMM_X_END, FMM_X_CHILD, FMM_X_NCHILD,
+ FMM_X_PARENT, FMM_X_CENTER, FMM_X_P2P, FMM_X_M2L, FMM_X_M, FMM_X_L, FMM_X_GEOM) = range(15)
+
+EXPORTED = ("fmm_setup", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
+            "fmm_set_timing", "fmm_export", "fmm_destroy", "fmm_last_error", "fmm_version")
+
+
+class FmmExec(C.Structure):
+    _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("rank", C.c_int), ("world_size", C.c_int)]
+
+
+class FmmStats(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("n_cells", C.c_int64), ("n_leaves", C.c_int64), ("n_p2p_pairs", C.c_int64),
+        ("n_m2l_pairs", C.c_int64), ("n_p2p_interactions", C.c_int64), ("own_begin", C.c_int64),
+        ("own_end", C.c_int64), ("p", C.c_int32), ("ncrit", C.c_int32), ("max_level", C.c_int32),
+        ("exponent", C.c_int32), ("theta", C.c_double), ("t_setup_ms", C.c_double * 8),
+        ("t_matvec_ms", C.c_double * 8), ("bytes_device", C.c_int64),
+    ]
+
+
+class FmmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"fmm status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1602_02244_b200.build` "
+                          "(the CUDA path has no fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, dp, i64 = C.c_void_p, C.c_void_p, C.c_int64
+    L.fmm_setup.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.POINTER(FmmExec)]
+    L.fmm_matvec.argtypes = [vp, dp, i64, dp, dp]
+    L.fmm_matvec_host.argtypes = [vp, dp, i64, dp, dp]
+    L.fmm_sync.argtypes = [vp]
+    L.fmm_direct.argtypes = [dp, dp, i64, dp, i64, dp, dp, C.POINTER(FmmExec)]
+    L.fmm_stats.argtypes = [vp, C.POINTER(FmmStats)]
+    L.fmm_set_timing.argtypes = [vp, C.c_int]
+    L.fmm_export.argtypes = [vp, C.c_int, vp, i64, C.POINTER(C.c_int64)]
+    L.fmm_destroy.argtypes = [vp]
+    L.fmm_destroy.restype = None
+    L.fmm_last_error.restype = C.c_char_p
+    L.fmm_version.restype = C.c_char_p
+    for nm in ("fmm_setup", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
+               "fmm_set_timing", "fmm_export"):
+        getattr(L, nm).restype = C.c_int
+    _lib = L
+    return L
+
+
+def check(status: int):
+    if status != FMM_OK:
+        raise FmmError(status, lib().fmm_last_error().decode())

@@ -1,0 +1,390 @@
+// api.cu — the C ABI of include/fmm.h: argument validation, plan lifecycle,
+// stage orchestration on the caller's stream, error mapping. Every exported
+// function catches all exceptions and returns an fmm_status (never aborts).
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "plan.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+fmm_status fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return (fmm_status)status;
+}
+
+template <typename F>
+fmm_status guarded(fmm_plan_s* P, F&& body) {
+  try {
+    body();
+    return FMM_OK;
+  } catch (const fmm::Error& e) {
+    if (P && e.status != FMM_ERR_USAGE && e.status != FMM_ERR_NUMERIC) P->poisoned = true;
+    return fail(e.status, e.what());
+  } catch (const std::bad_alloc&) {
+    if (P) P->poisoned = true;
+    return fail(FMM_ERR_OOM, "host allocation failed");
+  } catch (const std::exception& e) {
+    if (P) P->poisoned = true;
+    return fail(FMM_ERR_CUDA, e.what());
+  }
+}
+
+void usage(bool ok, const char* msg) {
+  if (!ok) throw fmm::Error(FMM_ERR_USAGE, msg);
+}
+
+// leaves sorted by their first particle (Morton order of the particle ranges)
+__global__ void leaf_keys_kernel(const int32_t* __restrict__ leaves, const int32_t* __restrict__ cbeg, int64_t nl,
+                                 uint64_t* __restrict__ k, uint32_t* __restrict__ v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nl) {
+    k[i] = (uint64_t)(uint32_t)cbeg[leaves[i]];
+    v[i] = (uint32_t)leaves[i];
+  }
+}
+
+__global__ void leaf_store_kernel(const uint32_t* __restrict__ v, int64_t nl, int32_t* __restrict__ leaves) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nl) leaves[i] = (int32_t)v[i];
+}
+
+void order_leaves_by_position(fmm_plan_s& P) {
+  const int64_t nl = P.nleaves;
+  if (nl <= 1) return;
+  fmm::DevBuf<uint64_t> k;
+  fmm::DevBuf<uint32_t> v;
+  k.alloc(nl);
+  v.alloc(nl);
+  leaf_keys_kernel<<<fmm::cdiv(nl, 256), 256, 0, P.stream>>>(P.leaves, P.cells.begin, nl, k, v);
+  FMM_LAUNCHED("leaf_keys_kernel");
+  int bits = 1;
+  while (((int64_t)1 << bits) < P.n) ++bits;
+  fmm::radix_sort_pairs(k, v, nl, bits, P.stream);
+  leaf_store_kernel<<<fmm::cdiv(nl, 256), 256, 0, P.stream>>>(v, nl, P.leaves);
+  FMM_LAUNCHED("leaf_store_kernel");
+}
+
+// This rank's targets: a contiguous range of leaves in Morton order with about
+// n / world particles each (cut at leaf boundaries).
+void choose_own_range(fmm_plan_s& P) {
+  if (P.world == 1) {
+    P.own_leaf_begin = 0;
+    P.own_leaf_end = P.nleaves;
+    P.own_begin = 0;
+    P.own_end = P.n;
+    return;
+  }
+  std::vector<int32_t> lv(P.nleaves), lb(P.cells.n);
+  FMM_CUDA(cudaMemcpyAsync(lv.data(), P.leaves.ptr, sizeof(int32_t) * P.nleaves, cudaMemcpyDeviceToHost, P.stream));
+  FMM_CUDA(cudaMemcpyAsync(lb.data(), P.cells.begin.ptr, sizeof(int32_t) * P.cells.n, cudaMemcpyDeviceToHost,
+                           P.stream));
+  FMM_CUDA(cudaStreamSynchronize(P.stream));
+  auto cut = [&](int r) -> int64_t {  // first leaf whose begin >= r * n / world
+    const int64_t target = (int64_t)r * P.n / P.world;
+    int64_t lo = 0, hi = P.nleaves;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) / 2;
+      if (lb[lv[mid]] < target)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    return lo;
+  };
+  P.own_leaf_begin = cut(P.rank);
+  P.own_leaf_end = cut(P.rank + 1);
+  P.own_begin = P.own_leaf_begin < P.nleaves ? lb[lv[P.own_leaf_begin]] : P.n;
+  P.own_end = P.own_leaf_end < P.nleaves ? lb[lv[P.own_leaf_end]] : P.n;
+}
+
+struct Timer {
+  fmm_plan_s& P;
+  bool on;
+  explicit Timer(fmm_plan_s& p, bool enable) : P(p), on(enable) {
+    if (on && !P.ev[0])
+      for (auto& e : P.ev) FMM_CUDA(cudaEventCreate(&e));
+  }
+  void mark(int i) {
+    if (on) FMM_CUDA(cudaEventRecord(P.ev[i], P.stream));
+  }
+  float between(int a, int b) {
+    float ms = 0;
+    FMM_CUDA(cudaEventElapsedTime(&ms, P.ev[a], P.ev[b]));
+    return ms;
+  }
+};
+
+void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
+  Timer T(P, P.timing);
+  T.mark(0);
+  fmm::gather_charges(P, q);
+  fmm::upward(P);
+  T.mark(1);
+  fmm::m2l_pass(P);
+  T.mark(2);
+  fmm::downward(P);
+  T.mark(3);
+  if (P.world > 1) {
+    FMM_CUDA(cudaMemsetAsync(phi, 0, sizeof(double) * P.n, P.stream));
+    if (grad) FMM_CUDA(cudaMemsetAsync(grad, 0, sizeof(double) * 3 * P.n, P.stream));
+  }
+  fmm::near_pass(P, q, phi, grad);
+  T.mark(4);
+  if (T.on) {
+    FMM_CUDA(cudaEventSynchronize(P.ev[4]));
+    P.t_matvec[FMM_T_UPWARD] = T.between(0, 1);
+    P.t_matvec[FMM_T_M2L] = T.between(1, 2);
+    P.t_matvec[FMM_T_DOWNWARD] = T.between(2, 3);
+    P.t_matvec[FMM_T_NEAR] = T.between(3, 4);
+    P.t_matvec[FMM_T_MATVEC_TOTAL] = T.between(0, 4);
+  }
+}
+
+void check_flags(fmm_plan_s& P) {
+  int32_t f = 0;
+  FMM_CUDA(cudaMemcpyAsync(&f, P.flags.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, P.stream));
+  FMM_CUDA(cudaStreamSynchronize(P.stream));
+  if (f) {
+    FMM_CUDA(cudaMemsetAsync(P.flags.ptr, 0, sizeof(int32_t), P.stream));
+    throw fmm::Error(FMM_ERR_NUMERIC, "fmm_matvec: non-finite charge");
+  }
+}
+
+}  // namespace
+
+int64_t fmm_plan_s::bytes() const {
+  int64_t b = keys.bytes() + perm.bytes() + pos.bytes() + leaves.bytes() + M.bytes() + L.bytes() + flags.bytes();
+  b += cells.level.bytes() + cells.begin.bytes() + cells.end.bytes() + cells.child.bytes() + cells.nchild.bytes() +
+       cells.parent.bytes() + cells.anchor.bytes() + cells.center.bytes();
+  b += p2p.tgt.bytes() + p2p.src.bytes() + p2p.off.bytes() + m2l.tgt.bytes() + m2l.src.bytes() + m2l.off.bytes();
+  b += host_stage_q.bytes() + host_stage_phi.bytes() + host_stage_grad.bytes();
+  return b;
+}
+
+extern "C" {
+
+fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncrit, double theta,
+                     const fmm_exec* ex) {
+  if (!out) return fail(FMM_ERR_USAGE, "fmm_setup: out is NULL");
+  *out = nullptr;
+  fmm_plan_s* P = nullptr;
+  fmm_status st = guarded(nullptr, [&] {
+    usage(ex != nullptr, "fmm_setup: ex is NULL");
+    usage(xyz != nullptr, "fmm_setup: xyz is NULL");
+    usage(n >= 1 && n < ((int64_t)1 << 31) - 1, "fmm_setup: n must be in [1, 2^31 - 2]");
+    usage(p >= 0 && p <= fmm::kMaxP, "fmm_setup: p must be in [0, 16]");
+    usage(ncrit >= 1, "fmm_setup: ncrit must be >= 1");
+    usage(theta > 0.0 && theta * theta * 3.0 < 1.0, "fmm_setup: theta must be in (0, 1/sqrt(3))");
+    usage(ex->world_size >= 1 && ex->rank >= 0 && ex->rank < ex->world_size, "fmm_setup: bad rank / world_size");
+    FMM_CUDA(cudaSetDevice(ex->device));
+    P = new fmm_plan_s();
+    P->device = ex->device;
+    P->stream = (cudaStream_t)ex->stream;
+    P->rank = ex->rank;
+    P->world = ex->world_size;
+    P->n = n;
+    P->p = p;
+    P->ncrit = ncrit;
+    P->nc = fmm::ncoef(p);
+    P->theta = theta;
+    P->theta2 = theta * theta;
+    cudaEvent_t e0, e1, e2, e3;
+    FMM_CUDA(cudaEventCreate(&e0));
+    FMM_CUDA(cudaEventCreate(&e1));
+    FMM_CUDA(cudaEventCreate(&e2));
+    FMM_CUDA(cudaEventCreate(&e3));
+    FMM_CUDA(cudaEventRecord(e0, P->stream));
+    fmm::build_tree(*P, xyz);
+    FMM_CUDA(cudaEventRecord(e1, P->stream));
+    fmm::traverse(*P);
+    FMM_CUDA(cudaEventRecord(e2, P->stream));
+    order_leaves_by_position(*P);
+    choose_own_range(*P);
+    P->M.alloc(P->cells.n * P->nc);
+    P->L.alloc(P->cells.n * P->nc);
+    FMM_CUDA(cudaEventRecord(e3, P->stream));
+    FMM_CUDA(cudaEventSynchronize(e3));
+    float a = 0, b = 0, c = 0;
+    FMM_CUDA(cudaEventElapsedTime(&a, e0, e1));
+    FMM_CUDA(cudaEventElapsedTime(&b, e1, e2));
+    FMM_CUDA(cudaEventElapsedTime(&c, e0, e3));
+    P->t_setup[FMM_T_TREE] = a;
+    P->t_setup[FMM_T_TRAVERSE] = b;
+    P->t_setup[FMM_T_SETUP_TOTAL] = c;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaEventDestroy(e3);
+  });
+  if (st != FMM_OK) {
+    delete P;
+    return st;
+  }
+  *out = P;
+  return FMM_OK;
+}
+
+fmm_status fmm_matvec(fmm_plan P, const double* q, int64_t n, double* phi, double* grad) {
+  if (!P) return fail(FMM_ERR_USAGE, "fmm_matvec: plan is NULL");
+  if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_matvec: plan is poisoned by an earlier error");
+  return guarded(P, [&] {
+    usage(n == P->n, "fmm_matvec: n differs from the setup n");
+    usage(q != nullptr && phi != nullptr, "fmm_matvec: q / phi is NULL");
+    FMM_CUDA(cudaSetDevice(P->device));
+    run_matvec(*P, q, phi, grad);
+  });
+}
+
+fmm_status fmm_matvec_host(fmm_plan P, const double* q_host, int64_t n, double* phi_host, double* grad_host) {
+  if (!P) return fail(FMM_ERR_USAGE, "fmm_matvec_host: plan is NULL");
+  if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_matvec_host: plan is poisoned by an earlier error");
+  return guarded(P, [&] {
+    usage(n == P->n, "fmm_matvec_host: n differs from the setup n");
+    usage(q_host != nullptr && phi_host != nullptr, "fmm_matvec_host: q / phi is NULL");
+    FMM_CUDA(cudaSetDevice(P->device));
+    if (P->host_stage_q.count < n) P->host_stage_q.alloc(n);
+    if (P->host_stage_phi.count < n) P->host_stage_phi.alloc(n);
+    if (grad_host && P->host_stage_grad.count < 3 * n) P->host_stage_grad.alloc(3 * n);
+    FMM_CUDA(cudaMemcpyAsync(P->host_stage_q.ptr, q_host, sizeof(double) * n, cudaMemcpyHostToDevice, P->stream));
+    double* dg = grad_host ? P->host_stage_grad.ptr : nullptr;
+    run_matvec(*P, P->host_stage_q.ptr, P->host_stage_phi.ptr, dg);
+    FMM_CUDA(cudaMemcpyAsync(phi_host, P->host_stage_phi.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, P->stream));
+    if (grad_host)
+      FMM_CUDA(cudaMemcpyAsync(grad_host, dg, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, P->stream));
+    check_flags(*P);
+  });
+}
+
+fmm_status fmm_sync(fmm_plan P) {
+  if (!P) return fail(FMM_ERR_USAGE, "fmm_sync: plan is NULL");
+  if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_sync: plan is poisoned by an earlier error");
+  return guarded(P, [&] {
+    FMM_CUDA(cudaSetDevice(P->device));
+    FMM_CUDA(cudaGetLastError());
+    check_flags(*P);
+  });
+}
+
+fmm_status fmm_direct(const double* src, const double* q, int64_t ns, const double* tgt, int64_t nt, double* phi,
+                      double* grad, const fmm_exec* ex) {
+  return guarded(nullptr, [&] {
+    usage(ex != nullptr, "fmm_direct: ex is NULL");
+    usage(ns >= 0 && nt >= 0, "fmm_direct: negative size");
+    usage(ns == 0 || (src && q), "fmm_direct: src / q is NULL");
+    usage(nt == 0 || (tgt && phi), "fmm_direct: tgt / phi is NULL");
+    FMM_CUDA(cudaSetDevice(ex->device));
+    fmm::launch_direct(src, q, ns, tgt, nt, phi, grad, (cudaStream_t)ex->stream);
+  });
+}
+
+fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
+  if (!P || !out) return fail(FMM_ERR_USAGE, "fmm_stats: NULL argument");
+  std::memset(out, 0, sizeof(*out));
+  out->n = P->n;
+  out->n_cells = P->cells.n;
+  out->n_leaves = P->nleaves;
+  out->n_p2p_pairs = P->p2p.n;
+  out->n_m2l_pairs = P->m2l.n;
+  out->n_p2p_interactions = P->n_p2p_interactions;
+  out->own_begin = P->own_begin;
+  out->own_end = P->own_end;
+  out->p = P->p;
+  out->ncrit = P->ncrit;
+  out->max_level = P->max_level;
+  out->exponent = P->e;
+  out->theta = P->theta;
+  for (int i = 0; i < 8; ++i) {
+    out->t_setup_ms[i] = P->t_setup[i];
+    out->t_matvec_ms[i] = P->t_matvec[i];
+  }
+  out->bytes_device = P->bytes();
+  return FMM_OK;
+}
+
+fmm_status fmm_set_timing(fmm_plan P, int enable) {
+  if (!P) return fail(FMM_ERR_USAGE, "fmm_set_timing: plan is NULL");
+  P->timing = enable != 0;
+  return FMM_OK;
+}
+
+fmm_status fmm_export(fmm_plan P, int what, void* dst, int64_t capacity, int64_t* count) {
+  if (!P || !count) return fail(FMM_ERR_USAGE, "fmm_export: NULL argument");
+  return guarded(P, [&] {
+    const void* src = nullptr;
+    int64_t cnt = 0, esz = 0;
+    std::vector<double> geom;
+    const int64_t nc = P->cells.n;
+    switch (what) {
+      case FMM_X_KEYS: src = P->keys.ptr; cnt = P->n; esz = 8; break;
+      case FMM_X_PERM: src = P->perm.ptr; cnt = P->n; esz = 4; break;
+      case FMM_X_LEVEL: src = P->cells.level.ptr; cnt = nc; esz = 4; break;
+      case FMM_X_ANCHOR: src = P->cells.anchor.ptr; cnt = 3 * nc; esz = 4; break;
+      case FMM_X_BEGIN: src = P->cells.begin.ptr; cnt = nc; esz = 4; break;
+      case FMM_X_END: src = P->cells.end.ptr; cnt = nc; esz = 4; break;
+      case FMM_X_CHILD: src = P->cells.child.ptr; cnt = nc; esz = 4; break;
+      case FMM_X_NCHILD: src = P->cells.nchild.ptr; cnt = nc; esz = 4; break;
+      case FMM_X_PARENT: src = P->cells.parent.ptr; cnt = nc; esz = 4; break;
+      case FMM_X_CENTER: src = nullptr; cnt = 3 * nc; esz = 8; break;
+      case FMM_X_P2P: src = nullptr; cnt = 2 * P->p2p.n; esz = 4; break;
+      case FMM_X_M2L: src = nullptr; cnt = 2 * P->m2l.n; esz = 4; break;
+      case FMM_X_M: src = P->M.ptr; cnt = 2 * nc * P->nc; esz = 8; break;
+      case FMM_X_L: src = P->L.ptr; cnt = 2 * nc * P->nc; esz = 8; break;
+      case FMM_X_GEOM:
+        geom = {P->lo[0], P->lo[1], P->lo[2], P->S, P->scale};
+        cnt = 5;
+        esz = 8;
+        break;
+      default: usage(false, "fmm_export: unknown array");
+    }
+    *count = cnt;
+    if (!dst) return;
+    usage(capacity >= cnt, "fmm_export: capacity too small");
+    FMM_CUDA(cudaSetDevice(P->device));
+    FMM_CUDA(cudaStreamSynchronize(P->stream));
+    if (what == FMM_X_GEOM) {
+      std::memcpy(dst, geom.data(), sizeof(double) * 5);
+    } else if (what == FMM_X_CENTER) {
+      std::vector<double4> c(nc);
+      FMM_CUDA(cudaMemcpy(c.data(), P->cells.center.ptr, sizeof(double4) * nc, cudaMemcpyDeviceToHost));
+      double* d = (double*)dst;
+      for (int64_t i = 0; i < nc; ++i) {
+        d[3 * i] = c[i].x;
+        d[3 * i + 1] = c[i].y;
+        d[3 * i + 2] = c[i].z;
+      }
+    } else if (what == FMM_X_P2P || what == FMM_X_M2L) {
+      const fmm::PairList& L = what == FMM_X_P2P ? P->p2p : P->m2l;
+      std::vector<int32_t> t(L.n), s(L.n);
+      if (L.n) {
+        FMM_CUDA(cudaMemcpy(t.data(), L.tgt.ptr, sizeof(int32_t) * L.n, cudaMemcpyDeviceToHost));
+        FMM_CUDA(cudaMemcpy(s.data(), L.src.ptr, sizeof(int32_t) * L.n, cudaMemcpyDeviceToHost));
+      }
+      int32_t* d = (int32_t*)dst;
+      for (int64_t i = 0; i < L.n; ++i) {
+        d[2 * i] = t[i];
+        d[2 * i + 1] = s[i];
+      }
+    } else if (cnt > 0) {
+      FMM_CUDA(cudaMemcpy(dst, src, esz * cnt, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+void fmm_destroy(fmm_plan P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  cudaStreamSynchronize(P->stream);
+  for (auto& e : P->ev)
+    if (e) cudaEventDestroy(e);
+  delete P;
+}
+
+const char* fmm_last_error(void) { return g_last_error.c_str(); }
+
+const char* fmm_version(void) { return "fmm-b200 0.1 (sm_100a, fp64)"; }
+
+}  // extern "C"

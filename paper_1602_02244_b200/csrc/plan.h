@@ -1,0 +1,134 @@
+// plan.h — the internal state behind the opaque fmm_plan of include/fmm.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <utility>
+#include <vector>
+
+#include "../../include/fmm.h"
+#include "common.cuh"
+
+namespace fmm {
+
+// Owning device buffer (cudaMalloc / cudaFree), byte accounting in the plan.
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  int64_t count = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count) { o.ptr = nullptr; o.count = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(ptr, o.ptr);
+    std::swap(count, o.count);
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    count = 0;
+  }
+  void alloc(int64_t n) {
+    release();
+    if (n > 0) FMM_CUDA(cudaMalloc(&ptr, sizeof(T) * n));
+    count = n;
+  }
+  // grow to at least n elements keeping the first `keep` elements
+  void grow(int64_t n, int64_t keep, cudaStream_t s) {
+    if (n <= count) return;
+    T* np = nullptr;
+    FMM_CUDA(cudaMalloc(&np, sizeof(T) * n));
+    if (ptr && keep > 0) FMM_CUDA(cudaMemcpyAsync(np, ptr, sizeof(T) * keep, cudaMemcpyDeviceToDevice, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    if (ptr) cudaFree(ptr);
+    ptr = np;
+    count = n;
+  }
+  int64_t bytes() const { return count * (int64_t)sizeof(T); }
+  operator T*() const { return ptr; }
+};
+
+// Cells in breadth-first (level, Morton) order: level_begin[l] .. level_begin[l+1].
+struct Cells {
+  DevBuf<int32_t> level, begin, end, child, nchild, parent;
+  DevBuf<int32_t> anchor;  // [3 * n]
+  DevBuf<double4> center;  // x, y, z, half side h (normalised frame)
+  int64_t n = 0, cap = 0;
+  void reserve(int64_t c, cudaStream_t s);
+};
+
+// Pair list grouped by target: src[off[t] .. off[t+1]) are the sources of cell t.
+struct PairList {
+  DevBuf<int32_t> tgt, src;  // [npairs]
+  DevBuf<int32_t> off;       // [ncells + 1]
+  int64_t n = 0;
+};
+
+}  // namespace fmm
+
+struct fmm_plan_s {
+  // execution context
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  bool poisoned = false;
+  bool timing = false;
+
+  // problem
+  int64_t n = 0;
+  int p = 0, ncrit = 0, nc = 0;
+  double theta = 0, theta2 = 0;
+  int e = 0;               // exact normalisation: coordinates are multiplied by 2^-e
+  double lo[3] = {0, 0, 0};
+  double S = 1, scale = 1; // normalised cube side and 2^21 / S
+
+  // particles in Morton order
+  fmm::DevBuf<uint64_t> keys;
+  fmm::DevBuf<uint32_t> perm;  // sorted position -> input index
+  fmm::DevBuf<double4> pos;    // x, y, z (normalised), q (filled per matvec)
+
+  // tree
+  fmm::Cells cells;
+  std::vector<int64_t> level_begin;  // host, size max_level + 2
+  int max_level = 0;
+  int64_t nleaves = 0;
+  fmm::DevBuf<int32_t> leaves;       // indices of leaf cells (ascending)
+
+  // interaction lists (dual tree traversal)
+  fmm::PairList p2p, m2l;
+  int64_t n_p2p_interactions = 0;
+
+  // this rank's targets (Morton range of sorted positions) and its leaves
+  int64_t own_begin = 0, own_end = 0;
+  int64_t own_leaf_begin = 0, own_leaf_end = 0;  // range in `leaves`
+
+  // expansions [ncells][nc] complex (m >= 0), normalised frame
+  fmm::DevBuf<double2> M, L;
+
+  // device status word: bit 0 = non-finite charge seen
+  fmm::DevBuf<int32_t> flags;
+  fmm::DevBuf<double> host_stage_q, host_stage_phi, host_stage_grad;  // fmm_matvec_host buffers
+
+  double t_setup[8] = {0};
+  double t_matvec[8] = {0};
+  cudaEvent_t ev[8] = {nullptr};
+
+  int64_t bytes() const;
+};
+
+namespace fmm {
+// setup stages (tree.cu, traverse.cu)
+void build_tree(fmm_plan_s& P, const double* xyz);
+void traverse(fmm_plan_s& P);
+// matvec stages (expansions.cu, near.cu)
+void upward(fmm_plan_s& P);
+void m2l_pass(fmm_plan_s& P);
+void downward(fmm_plan_s& P);
+void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
+void gather_charges(fmm_plan_s& P, const double* q);
+void launch_direct(const double* src, const double* q, int64_t ns, const double* tgt, int64_t nt,
+                   double* phi, double* grad, cudaStream_t s);
+}  // namespace fmm

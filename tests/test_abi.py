@@ -1,0 +1,76 @@
+"""The C-ABI library loads and exports every symbol include/fmm.h declares (no GPU needed).
+Also: the product package never imports the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "fmm.h")).read()
+    return sorted(set(re.findall(r"FMM_API\s+[\w\s\*]+?\b(fmm_\w+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def libfmm():
+    from paper_1602_02244_b200 import build
+
+    path = build.build()
+    return ctypes.CDLL(path)
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("fmm_setup", "fmm_matvec", "fmm_direct", "fmm_matvec_host", "fmm_destroy", "fmm_last_error"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(libfmm):
+    for s in declared_symbols():
+        assert hasattr(libfmm, s), s
+    out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_1602_02244_b200", "libfmm.so")],
+                         capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (fmm_\w+)", out))
+    assert exported == set(declared_symbols())
+
+
+def test_python_binding_names_match(libfmm):
+    from paper_1602_02244_b200 import _native
+
+    assert set(_native.EXPORTED) == set(declared_symbols())
+    assert _native.lib().fmm_version().decode().startswith("fmm-b200")
+
+
+def test_library_is_sm100a_cubin():
+    out = subprocess.run(["cuobjdump", "--list-elf", os.path.join(ROOT, "paper_1602_02244_b200", "libfmm.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_usage_errors_need_no_gpu(libfmm):
+    """Argument validation happens before any device work (fmm.h error table)."""
+    from paper_1602_02244_b200 import _native as N
+
+    L = N.lib()
+    h = ctypes.c_void_p()
+    ex = N.FmmExec(0, None, 0, 1)
+    assert L.fmm_setup(ctypes.byref(h), None, 10, 4, 8, 0.4, ctypes.byref(ex)) == N.FMM_ERR_USAGE
+    assert b"NULL" in L.fmm_last_error()
+    dummy = ctypes.c_void_p(1)
+    for args in ((0, 4, 8, 0.4), (10, -1, 8, 0.4), (10, 17, 8, 0.4), (10, 4, 0, 0.4), (10, 4, 8, 0.0),
+                 (10, 4, 8, 0.58)):
+        assert L.fmm_setup(ctypes.byref(h), dummy, *args, ctypes.byref(ex)) == N.FMM_ERR_USAGE
+    assert L.fmm_matvec(None, None, 0, None, None) == N.FMM_ERR_USAGE
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1602_02244_b200")
+    pat = re.compile(r"(import\s+oracle|from\s+oracle|liboracle|fmm_oracle|oracle\.oracle)")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                assert not pat.search(open(os.path.join(dp, f)).read()), f

@@ -72,6 +72,18 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
     return LIB
 
 
+PROBE_SRC = os.path.join(ROOT, "tools", "fp64_probe.cu")
+PROBE_LIB = os.path.join(ROOT, "tools", "libfp64probe.so")
+
+
+def build_tools(force: bool = False) -> str:
+    """Measurement-only helper (FP64 roofline probe used by bench.py), same arch flags."""
+    if force or not os.path.exists(PROBE_LIB) or os.path.getmtime(PROBE_LIB) < os.path.getmtime(PROBE_SRC):
+        subprocess.check_call([NVCC, *NVFLAGS, "-shared", PROBE_SRC, "-o", PROBE_LIB])
+    return PROBE_LIB
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, ptxas_verbose="--ptxas" in sys.argv)
+    build_tools(force="--force" in sys.argv)
     print(LIB)

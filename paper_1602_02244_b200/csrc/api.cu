@@ -2,6 +2,7 @@
 // stage orchestration on the caller's stream, error mapping. Every exported
 // function catches all exceptions and returns an fmm_status (never aborts).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -124,9 +125,12 @@ void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
   fmm::gather_charges(P, q);
   fmm::upward(P);
   T.mark(1);
-  fmm::m2l_pass(P);
+  if (P.m2l_variant == 2)
+    fmm::m2l_dmma_pass(P);
+  else
+    fmm::m2l_pass(P);
   T.mark(2);
-  fmm::downward(P);
+  if (!P.debug_skip_l2l) fmm::downward(P);
   T.mark(3);
   if (P.world > 1) {
     FMM_CUDA(cudaMemsetAsync(phi, 0, sizeof(double) * P.n, P.stream));
@@ -162,6 +166,7 @@ int64_t fmm_plan_s::bytes() const {
        cells.parent.bytes() + cells.anchor.bytes() + cells.center.bytes();
   b += p2p.tgt.bytes() + p2p.src.bytes() + p2p.off.bytes() + m2l.tgt.bytes() + m2l.src.bytes() + m2l.off.bytes();
   b += host_stage_q.bytes() + host_stage_phi.bytes() + host_stage_grad.bytes();
+  b += m2l_dmma.bytes();
   return b;
 }
 
@@ -204,6 +209,11 @@ fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncr
     FMM_CUDA(cudaEventRecord(e2, P->stream));
     order_leaves_by_position(*P);
     choose_own_range(*P);
+    const char* v = getenv("FMM_M2L_VARIANT");
+    if (v && v[0] == '1') P->m2l_variant = 1;
+    const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // test hook: export M2L-only local expansions
+    P->debug_skip_l2l = dbg && dbg[0] == '1';
+    if (P->m2l_variant == 2) fmm::m2l_dmma_setup(*P);
     P->M.alloc(P->cells.n * P->nc);
     P->L.alloc(P->cells.n * P->nc);
     FMM_CUDA(cudaEventRecord(e3, P->stream));

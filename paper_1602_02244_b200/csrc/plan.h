@@ -67,6 +67,25 @@ struct PairList {
   int64_t n = 0;
 };
 
+// M2L v2 state (m2l_dmma.cu): canonical operator classes, tiles, chunks.
+struct M2LDmma {
+  int NR = 0, NRpad = 0, nmt = 0, Kpad = 0, nks = 0, NC = 0, T = 0, ystride = 0;
+  int64_t nclass = 0, ntiles = 0, nchunks = 0, npairs = 0;
+  DevBuf<double> ops;          // [nclass][nmt][nks][32] A fragments
+  DevBuf<int32_t> col_src;     // [npairs] source cell per GEMM column
+  DevBuf<int32_t> col_meta;    // [npairs] slot | g << 8
+  DevBuf<int32_t> chunk_begin; // [nchunks + 1]
+  DevBuf<int32_t> chunk_class; // [nchunks]
+  DevBuf<int32_t> tile_chunk;  // [ntiles + 1]
+  DevBuf<int32_t> tile_cells;  // [ntiles * T], -1 padding
+  DevBuf<int32_t> symtab;      // [16][2][NR]
+  DevBuf<double> hpow;         // [22][p + 2]
+  int64_t bytes() const {
+    return ops.bytes() + col_src.bytes() + col_meta.bytes() + chunk_begin.bytes() + chunk_class.bytes() +
+           tile_chunk.bytes() + tile_cells.bytes() + symtab.bytes() + hpow.bytes();
+  }
+};
+
 }  // namespace fmm
 
 struct fmm_plan_s {
@@ -76,6 +95,7 @@ struct fmm_plan_s {
   int rank = 0, world = 1;
   bool poisoned = false;
   bool timing = false;
+  bool debug_skip_l2l = false;
 
   // problem
   int64_t n = 0;
@@ -100,6 +120,8 @@ struct fmm_plan_s {
   // interaction lists (dual tree traversal)
   fmm::PairList p2p, m2l;
   int64_t n_p2p_interactions = 0;
+  fmm::M2LDmma m2l_dmma;
+  int m2l_variant = 2;  // 1 = matrix-free O(p^4) per pair (v1), 2 = DMMA operator classes (v2)
 
   // this rank's targets (Morton range of sorted positions) and its leaves
   int64_t own_begin = 0, own_end = 0;
@@ -126,6 +148,8 @@ void traverse(fmm_plan_s& P);
 // matvec stages (expansions.cu, near.cu)
 void upward(fmm_plan_s& P);
 void m2l_pass(fmm_plan_s& P);
+void m2l_dmma_setup(fmm_plan_s& P);
+void m2l_dmma_pass(fmm_plan_s& P);
 void downward(fmm_plan_s& P);
 void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
 void gather_charges(fmm_plan_s& P, const double* q);

@@ -30,6 +30,7 @@
 //    memory and added to the accumulators by one thread per (row, slot
 //    parity) in column order: deterministic, no atomics.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "harmonics.cuh"
@@ -324,130 +325,200 @@ struct M2LArgs {
   const int32_t* col_meta;
   const int32_t* chunk_begin;
   const int32_t* chunk_class;
+  const int32_t* chunk_seg;  // [nchunks + 1] first slot segment of each chunk
+  const int32_t* seg_begin;  // [nseg + 1] first column of each segment (global index)
   const int32_t* tile_chunk;
   const int32_t* tile_cells;
   const int32_t* symtab;  // [16][2][NR]
   const double* hpow;     // [22][p+2]
   const int32_t* level;
-  const double2* M;
+  const double* Mt;       // [ncells][Kpad] scaled real-form multipoles
   double2* L;
   int p, nc, NR, NRpad, Kpad, nks, nmt, T, NC, ystride;
 };
 
-// one CTA per tile; blockDim = 32 * nmt / 2 (each warp owns two 8-row m-tiles)
-__global__ void __launch_bounds__(640, 1) m2l_dmma_kernel(const M2LArgs a) {
-  extern __shared__ double sm[];
-  const int NR = a.NR, T = a.T, NC = a.NC;
-  double* acc = sm;                                                       // [T][NR]
-  double* xy = acc + (size_t)T * NR;                                      // X frags / Y staging
-  int32_t* meta = (int32_t*)(xy + (size_t)max(a.Kpad * NC, NC * a.ystride));  // [NC] slot | g << 8
-  int32_t* srcs = meta + NC;                                              // [NC]
-  int32_t* sym = srcs + NC;                                               // [16][2][NR]
-  int32_t* dec = sym + 32 * NR;                                           // [NR] cidx << 8 | n << 1 | part
-  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
-  const int tile = blockIdx.x;
-  for (int e = tid; e < T * NR; e += nthr) acc[e] = 0.0;
-  for (int e = tid; e < 32 * NR; e += nthr) sym[e] = a.symtab[e];
-  for (int r = tid; r < NR; r += nthr) {
+// S9 pre-pass: M~ rows in the real basis, M~[c][r] = {Re,Im} M_n^m(c) h_c^{-n}, zero for r >= NR.
+__global__ void mtilde_kernel(const double2* __restrict__ M, const int32_t* __restrict__ level,
+                              const double* __restrict__ hpow, int64_t ncells, int p, int nc, int NR, int Kpad,
+                              double* __restrict__ Mt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ncells * Kpad) return;
+  const int64_t c = e / Kpad;
+  const int r = (int)(e - c * Kpad);
+  double v = 0.0;
+  if (r < NR) {
     int n, m, part;
     real_decode(r, n, m, part);
-    dec[r] = (cidx(n, m) << 8) | (n << 1) | part;
+    const double2 z = M[c * nc + cidx(n, m)];
+    v = (part ? z.y : z.x) * hpow[level[c] * (p + 2) + n];
   }
-  const int ntn = NC / 8;
-  const int c_first = a.tile_chunk[tile], c_last = a.tile_chunk[tile + 1];
-  for (int ch = c_first; ch < c_last; ++ch) {
-    const int cls = a.chunk_class[ch];
-    const int cb = a.chunk_begin[ch];
-    const int ncol = a.chunk_begin[ch + 1] - cb;
-    __syncthreads();  // previous chunk's accumulate pass is done with xy / meta
-    for (int t = tid; t < NC; t += nthr) {  // blockDim may be < NC (p <= 3: one warp)
-      meta[t] = t < ncol ? a.col_meta[cb + t] : 0;
-      srcs[t] = t < ncol ? a.col_src[cb + t] : 0;
-    }
-    __syncthreads();
-    // ---- gather X~ (scaled, canonical frame) into B-fragment order: one warp per column
-    for (int col = warp; col < NC; col += nwarp) {
-      double* xcol = xy + (col >> 3) * 32 + (col & 7) * 4;
-      if (col < ncol) {
-        const int B = srcs[col];
-        const int32_t* symM = sym + (meta[col] >> 8) * 2 * NR;
-        const double* hp = a.hpow + a.level[B] * (a.p + 2);
-        const double* Mb = (const double*)(a.M + (int64_t)B * a.nc);
-        for (int k = lane; k < a.Kpad; k += 32) {
-          double v = 0.0;
-          if (k < NR) {
-            const int ent = symM[k];
-            const int d = dec[ent & 0xffff];
-            v = Mb[2 * (d >> 8) + (d & 1)] * hp[(d >> 1) & 0x7f];
-            if (ent >> 16) v = -v;
-          }
-          xcol[(k >> 2) * ntn * 32 + (k & 3)] = v;
+  Mt[e] = v;
+}
+
+// ---------------------------------------------------------------------------------------
+// Shared-memory layout of one chunk: X[col][k] (and later Y[col][row]) with a column stride
+// S = xstride, S % 16 == 4 doubles, so the DMMA B-fragment loads (8 columns x 4 rows per warp),
+// the column-wise gather stores and the staged-Y stores are all bank-conflict free.
+
+// C[2][NT] = A(two m-tiles, fragments streamed from L2, 3 k-steps of prefetch) x X(NT n-tiles)
+template <int NT>
+__device__ __forceinline__ void gemm_chunk(double (&c)[2][8][2], const double* __restrict__ A0, int nks,
+                                           const double* __restrict__ xc, int S, int lane) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+  const double* A1 = A0 + (int64_t)nks * 32;
+  constexpr int D = 3;
+  double ra0[D], ra1[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    ra0[d] = d < nks ? __ldg(A0 + d * 32) : 0.0;
+    ra1[d] = d < nks ? __ldg(A1 + d * 32) : 0.0;
+  }
+  const double* bx = xc + (lane >> 2) * S + (lane & 3);
+  for (int ks = 0; ks < nks; ks += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (ks + d < nks) {
+        const double a0 = ra0[d], a1 = ra1[d];
+        if (ks + d + D < nks) {
+          ra0[d] = __ldg(A0 + (ks + d + D) * 32);
+          ra1[d] = __ldg(A1 + (ks + d + D) * 32);
         }
-      } else {
-        for (int k = lane; k < a.Kpad; k += 32) xcol[(k >> 2) * ntn * 32 + (k & 3)] = 0.0;
-      }
-    }
-    __syncthreads();
-    // ---- GEMM on DMMA: warp owns m-tiles 2w, 2w+1 and all n-tiles
-    double c[2][8][2];
+        double bv[NT];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < NT; ++j) bv[j] = bx[j * 8 * S + 4 * (ks + d)];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) c[i][j][0] = c[i][j][1] = 0.0;
-    const int nta = (ncol + 7) >> 3;
-    const double* A0 = a.ops + (((int64_t)cls * a.nmt + 2 * warp) * a.nks) * 32 + lane;
-    const double* A1 = A0 + (int64_t)a.nks * 32;
-    double an0 = __ldg(A0), an1 = __ldg(A1);
-    for (int ks = 0; ks < a.nks; ++ks) {
-      const double a0 = an0, a1 = an1;
-      if (ks + 1 < a.nks) {  // prefetch next k-step's operator fragments
-        an0 = __ldg(A0 + (ks + 1) * 32);
-        an1 = __ldg(A1 + (ks + 1) * 32);
-      }
-      const double* bx = xy + (ks * ntn) * 32 + lane;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (j < nta) {
-          const double b = bx[j * 32];
-          dmma884(c[0][j][0], c[0][j][1], a0, b);
-          dmma884(c[1][j][0], c[1][j][1], a1, b);
+        for (int j = 0; j < NT; ++j) {
+          dmma884(c[0][j][0], c[0][j][1], a0, bv[j]);
+          dmma884(c[1][j][0], c[1][j][1], a1, bv[j]);
         }
-      }
-    }
-    __syncthreads();  // everyone is done reading X
-    // ---- stage Y[col][row]
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (j < nta) {
-          const int row = 16 * warp + 8 * i + (lane >> 2);
-          const int col = 8 * j + 2 * (lane & 3);
-          xy[col * a.ystride + row] = c[i][j][0];
-          xy[(col + 1) * a.ystride + row] = c[i][j][1];
-        }
-      }
-    __syncthreads();
-    // ---- accumulate: thread (row r, slot parity q) walks the columns in order
-    for (int t = tid; t < 2 * a.NRpad; t += nthr) {
-      const int r = t % a.NRpad, q = t / a.NRpad;
-      if (r >= NR) continue;
-      double* accr = acc + r;
-      for (int col = 0; col < ncol; ++col) {
-        const int mt_ = meta[col];
-        const int slot = mt_ & 0xff;
-        if ((slot & 1) != q) continue;
-        const int ent = sym[((mt_ >> 8) * 2 + 1) * NR + r];
-        const double y = xy[col * a.ystride + (ent & 0xffff)];
-        accr[slot * NR] += (ent >> 16) ? -y : y;
       }
     }
   }
-  __syncthreads();
-  // ---- write back L = L~ h_A^{-(j+1)} for the tile's targets (L was zeroed)
-  for (int e = tid; e < T * NR; e += nthr) {
+}
+
+__device__ __forceinline__ void gemm_dispatch(int nta, double (&c)[2][8][2], const double* A0, int nks,
+                                              const double* xc, int S, int lane) {
+  switch (nta) {
+    case 1: gemm_chunk<1>(c, A0, nks, xc, S, lane); break;
+    case 2: gemm_chunk<2>(c, A0, nks, xc, S, lane); break;
+    case 3: gemm_chunk<3>(c, A0, nks, xc, S, lane); break;
+    case 4: gemm_chunk<4>(c, A0, nks, xc, S, lane); break;
+    case 5: gemm_chunk<5>(c, A0, nks, xc, S, lane); break;
+    case 6: gemm_chunk<6>(c, A0, nks, xc, S, lane); break;
+    case 7: gemm_chunk<7>(c, A0, nks, xc, S, lane); break;
+    default: gemm_chunk<8>(c, A0, nks, xc, S, lane); break;
+  }
+}
+
+// Y[col][row] over the consumed X buffer (rows < NR only)
+__device__ __forceinline__ void stage_y(const double (&c)[2][8][2], double* xc, int S, int NR, int nta, int warp,
+                                        int lane) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int row = 16 * warp + 8 * i + (lane >> 2);
+      const int col = 8 * j + 2 * (lane & 3);
+      if (j < nta && row < NR) {
+        xc[col * S + row] = c[i][j][0];
+        xc[(col + 1) * S + row] = c[i][j][1];
+      }
+    }
+}
+
+// X[col][k] = (D^M_g)^{-1} M~_B[k] for the chunk's columns; one warp per column, 4 columns
+// in flight per warp; zero for k in [NR, Kpad) and for columns in [ncol, 8 * ceil(ncol / 8)).
+template <int U, int Q>  // U columns in flight per warp, Q * 32 >= Kpad rows
+__device__ __forceinline__ void gather_cols(double* xb, int ncol, const int32_t* meta, const int32_t* srcs,
+                                            const int32_t* sym, const double* __restrict__ Mt, int NR, int Kpad,
+                                            int S, int w, int nw, int lane) {
+  const int ncol8 = (ncol + 7) & ~7;
+  for (int c0 = w * U; c0 < ncol8; c0 += nw * U) {
+    double v[U][Q];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int col = c0 + u;
+      const bool live = col < ncol;
+      const int B = live ? srcs[col] : 0;
+      const int32_t* sm_ = sym + (live ? (meta[col] >> 8) : 0) * 2 * NR;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int k = lane + 32 * q;
+        v[u][q] = 0.0;
+        if (live && k < NR) {
+          const int ent = sm_[k];
+          const double x = __ldg(Mt + (int64_t)B * Kpad + (ent & 0xffff));
+          v[u][q] = (ent >> 16) ? -x : x;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int col = c0 + u;
+      if (col < ncol8) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int k = lane + 32 * q;
+          if (k < Kpad) xb[col * S + k] = v[u][q];
+        }
+      }
+    }
+  }
+}
+
+// per-row output transform for all 16 g: bit 2g = take the re/im partner row, bit 2g+1 = negate
+__device__ __forceinline__ uint32_t ltrans_mask(const int32_t* sym, int NR, int r, int& partner_off) {
+  uint32_t mask = 0;
+  partner_off = 0;
+  for (int g = 0; g < 16; ++g) {
+    const int ent = sym[(g * 2 + 1) * NR + r];
+    const int src = ent & 0xffff;
+    if (src != r) {
+      partner_off = src - r;
+      mask |= 1u << (2 * g);
+    }
+    if (ent >> 16) mask |= 2u << (2 * g);
+  }
+  return mask;
+}
+
+// acc[slot][r] += sum over the chunk's columns of (D^L_g Y)[r], segments [s_lo, s_hi) of this thread
+__device__ __forceinline__ void accumulate_rows(double* acc, const double* y, int S, int NR, int r, uint32_t mask,
+                                                int poff, const int32_t* meta, const int32_t* sb,
+                                                const int32_t* ss, int s_lo, int s_hi) {
+  for (int sgi = s_lo; sgi < s_hi; ++sgi) {
+    double* ap = acc + ss[sgi] * NR + r;
+    double v = *ap;
+    const int cb = sb[sgi], ce = sb[sgi + 1];
+    int col = cb;
+    for (; col + 2 <= ce; col += 2) {
+      const int g0 = meta[col] >> 8, g1 = meta[col + 1] >> 8;
+      const double y00 = y[col * S + r], y01 = y[col * S + r + poff];
+      const double y10 = y[(col + 1) * S + r], y11 = y[(col + 1) * S + r + poff];
+      const uint32_t m0 = mask >> (2 * g0), m1 = mask >> (2 * g1);
+      double t0 = (m0 & 1) ? y01 : y00, t1 = (m1 & 1) ? y11 : y10;
+      v += (m0 & 2) ? -t0 : t0;
+      v += (m1 & 2) ? -t1 : t1;
+    }
+    if (col < ce) {
+      const int g0 = meta[col] >> 8;
+      const uint32_t m0 = mask >> (2 * g0);
+      const double t0 = (m0 & 1) ? y[col * S + r + poff] : y[col * S + r];
+      v += (m0 & 2) ? -t0 : t0;
+    }
+    *ap = v;
+  }
+}
+
+__device__ __forceinline__ void writeback(const M2LArgs& a, const double* acc, const int32_t* dec, int tile, int tid,
+                                          int nthr) {
+  const int NR = a.NR;
+  for (int e = tid; e < a.T * NR; e += nthr) {
     const int slot = e / NR, r = e - slot * NR;
-    const int cell = a.tile_cells[tile * T + slot];
+    const int cell = a.tile_cells[tile * a.T + slot];
     if (cell < 0) continue;
     const int d = dec[r];
     const double v = acc[e] * a.hpow[a.level[cell] * (a.p + 2) + ((d >> 1) & 0x7f) + 1];
@@ -455,7 +526,317 @@ __global__ void __launch_bounds__(640, 1) m2l_dmma_kernel(const M2LArgs a) {
   }
 }
 
+// chunk metadata (columns + slot segments) into buffer slot b
+__device__ __forceinline__ void load_meta_dev(const M2LArgs& a, int ch, int32_t* meta, int32_t* srcs, int32_t* sslot,
+                                              int32_t* sbeg, int t0, int nt) {
+  const int cb = a.chunk_begin[ch], ncol = a.chunk_begin[ch + 1] - cb;
+  const int s0 = a.chunk_seg[ch], ns = a.chunk_seg[ch + 1] - s0;
+  for (int t = t0; t < a.NC; t += nt) {
+    meta[t] = t < ncol ? a.col_meta[cb + t] : 0;
+    srcs[t] = t < ncol ? a.col_src[cb + t] : 0;
+    if (t < ns) sslot[t] = a.col_meta[a.seg_begin[s0 + t]] & 0xff;
+  }
+  for (int t = t0; t <= ns; t += nt) sbeg[t] = a.seg_begin[s0 + t] - cb;
+}
+
+// shared-memory carve-up common to both kernels
+struct Smem {
+  double *acc, *x0, *x1;
+  int32_t *meta, *srcs, *sslot, *sbeg, *sym, *dec, *lmask, *lpoff;
+};
+__device__ __forceinline__ Smem carve(double* sm, const M2LArgs& a) {
+  Smem m;
+  const int xsz = a.NC * a.ystride;
+  m.acc = sm;
+  m.x0 = m.acc + (size_t)a.T * a.NR;
+  m.x1 = m.x0 + xsz;
+  m.meta = (int32_t*)(m.x1 + xsz);  // [2][NC]
+  m.srcs = m.meta + 2 * a.NC;       // [2][NC]
+  m.sslot = m.srcs + 2 * a.NC;      // [2][NC]
+  m.sbeg = m.sslot + 2 * a.NC;      // [2][NC + 1]
+  m.sym = m.sbeg + 2 * (a.NC + 1);  // [16][2][NR]
+  m.dec = m.sym + 32 * a.NR;        // [NR]
+  m.lmask = m.dec + a.NR;           // [NR] output-transform bits per row (ltrans_mask)
+  m.lpoff = m.lmask + a.NR;         // [NR] re/im partner offset per row
+  return m;
+}
+__device__ __forceinline__ void init_smem(const M2LArgs& a, const Smem& m, int tid, int nthr) {
+  for (int e = tid; e < a.T * a.NR; e += nthr) m.acc[e] = 0.0;
+  for (int e = tid; e < 32 * a.NR; e += nthr) m.sym[e] = a.symtab[e];
+  for (int r = tid; r < a.NR; r += nthr) {
+    int n, mm, part;
+    real_decode(r, n, mm, part);
+    m.dec[r] = (cidx(n, mm) << 8) | (n << 1) | part;
+  }
+  __syncthreads();  // sym complete
+  for (int r = tid; r < a.NR; r += nthr) {
+    int poff = 0;
+    m.lmask[r] = (int32_t)ltrans_mask(m.sym, a.NR, r, poff);
+    m.lpoff[r] = poff;
+  }
+}
+
+// all (row group, row) items of one chunk's accumulate, spread over nt threads starting at t0
+__device__ __forceinline__ void accumulate_chunk(const Smem& m, const double* y, int S, int NR, int ns,
+                                                 const int32_t* meta, const int32_t* sb, const int32_t* ss, int t0,
+                                                 int nt) {
+  const int RG = max(1, nt / NR);
+  for (int t = t0; t < RG * NR; t += nt) {
+    const int rg = t / NR, r = t - rg * NR;
+    accumulate_rows(m.acc, y, S, NR, r, (uint32_t)m.lmask[r], m.lpoff[r], meta, sb, ss, ns * rg / RG,
+                    ns * (rg + 1) / RG);
+  }
+}
+
+// Plain variant (all warps take every phase in turn): used where the warp-specialised one
+// does not fit (p <= 4: fewer than two rows of helpers; p >= 14: too many MMA warps).
+__global__ void __launch_bounds__(640, 1) m2l_dmma_kernel(const M2LArgs a) {
+  extern __shared__ double sm[];
+  const Smem m = carve(sm, a);
+  const int NR = a.NR, NC = a.NC, S = a.ystride;
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
+  const int tile = blockIdx.x;
+  init_smem(a, m, tid, nthr);
+  __syncthreads();
+  for (int ch = a.tile_chunk[tile]; ch < a.tile_chunk[tile + 1]; ++ch) {
+    const int cls = a.chunk_class[ch];
+    const int ncol = a.chunk_begin[ch + 1] - a.chunk_begin[ch];
+    __syncthreads();
+    load_meta_dev(a, ch, m.meta, m.srcs, m.sslot, m.sbeg, tid, nthr);
+    __syncthreads();
+    gather_cols<2, 10>(m.x0, ncol, m.meta, m.srcs, m.sym, a.Mt, NR, a.Kpad, S, warp, nwarp, lane);
+    __syncthreads();
+    const int nta = (ncol + 7) >> 3;
+    double c[2][8][2];
+    if (2 * warp < a.nmt) {
+      const double* A0 = a.ops + (((int64_t)cls * a.nmt + 2 * warp) * a.nks) * 32 + lane;
+      gemm_dispatch(nta, c, A0, a.nks, m.x0, S, lane);
+    }
+    __syncthreads();
+    if (2 * warp < a.nmt) stage_y(c, m.x0, S, NR, nta, warp, lane);
+    __syncthreads();
+    accumulate_chunk(m, m.x0, S, NR, a.chunk_seg[ch + 1] - a.chunk_seg[ch], m.meta, m.sbeg, m.sslot, tid, nthr);
+  }
+  __syncthreads();
+  writeback(a, m.acc, m.dec, tile, tid, nthr);
+}
+
+// ---------------------------------------------------------------------------------------
+// Warp-specialised variant: nmma = nmt/2 MMA warps run only the DMMA GEMMs; nhelp helper
+// warps gather the next chunk's X and add the previous chunk's Y into the accumulators.
+// Handshake with named barriers (ids alternate by chunk parity):
+//   Xfull(i):  helpers bar.arrive after storing X(i);  MMA bar.sync before GEMM(i)
+//   Yfull(i):  MMA bar.arrive after staging Y(i);      helpers bar.sync before adding Y(i)
+// Y(i) is staged over X[i % 2] (consumed by GEMM(i)); helpers overwrite X[i % 2] with
+// X(i+2) only after adding Y(i), so two X buffers suffice.
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(512, 1) m2l_ws_kernel(const M2LArgs a, int nmma, int nhelp, int dbg) {
+  extern __shared__ double sm[];
+  const Smem m = carve(sm, a);
+  const int NR = a.NR, NC = a.NC, S = a.ystride;
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;
+  const int nmma_t = 32 * nmma, nhelp_t = 32 * nhelp, nall = nmma_t + nhelp_t;
+  init_smem(a, m, tid, nthr);
+  const int c_first = a.tile_chunk[tile], c_last = a.tile_chunk[tile + 1];
+  __syncthreads();
+  if (warp >= nmma) {
+    // ================= helper warps
+    const int h = tid - nmma_t, hw = warp - nmma;
+    auto prep = [&](int ch, int b) {
+      load_meta_dev(a, ch, m.meta + b * NC, m.srcs + b * NC, m.sslot + b * NC, m.sbeg + b * (NC + 1), h, nhelp_t);
+      named_sync(6, nhelp_t);  // metadata visible to all helpers
+      if (!(dbg & 1))
+        gather_cols<4, 8>(b ? m.x1 : m.x0, a.chunk_begin[ch + 1] - a.chunk_begin[ch], m.meta + b * NC,
+                          m.srcs + b * NC, m.sym, a.Mt, NR, a.Kpad, S, hw, nhelp, lane);
+    };
+    if (c_first < c_last) {
+      prep(c_first, 0);
+      named_arrive(1, nall);  // Xfull(0)
+    }
+    for (int ch = c_first; ch < c_last; ++ch) {
+      const int i = ch - c_first, b = i & 1, nb = b ^ 1;
+      if (ch + 1 < c_last) {
+        prep(ch + 1, nb);
+        named_arrive(1 + nb, nall);  // Xfull(i+1)
+      }
+      named_sync(3 + b, nall);  // Yfull(i)
+      if (!(dbg & 2))
+        accumulate_chunk(m, b ? m.x1 : m.x0, S, NR, a.chunk_seg[ch + 1] - a.chunk_seg[ch], m.meta + b * NC,
+                         m.sbeg + b * (NC + 1), m.sslot + b * NC, h, nhelp_t);
+      named_sync(6, nhelp_t);  // helpers done with meta[b] / Y(i) before they are overwritten
+    }
+  } else {
+    // ================= MMA warps
+    for (int ch = c_first; ch < c_last; ++ch) {
+      const int i = ch - c_first, b = i & 1;
+      named_sync(1 + b, nall);  // Xfull(i)
+      double* xc = b ? m.x1 : m.x0;
+      const int cls = a.chunk_class[ch];
+      const int nta = (a.chunk_begin[ch + 1] - a.chunk_begin[ch] + 7) >> 3;
+      double c[2][8][2];
+      const double* A0 = a.ops + (((int64_t)cls * a.nmt + 2 * warp) * a.nks) * 32 + lane;
+      gemm_dispatch(nta, c, A0, a.nks, xc, S, lane);
+      named_sync(5, nmma_t);  // all MMA warps done reading X[b]
+      stage_y(c, xc, S, NR, nta, warp, lane);
+      named_arrive(3 + b, nall);  // Yfull(i)
+    }
+  }
+  __syncthreads();
+  writeback(a, m.acc, m.dec, tile, tid, nthr);
+}
+
+// ---------------------------------------------------------------------------------------
+// Compile-time-p version of the warp-specialised kernel (p = 5..14): all strides and loop
+// bounds are constants, so the DMMA loop unrolls with immediate shared-memory offsets.
+constexpr int ct_xstride(int kpad) {
+  int s = kpad;
+  while (s % 16 != 4) ++s;
+  return s;
+}
+template <int P>
+struct Geo {
+  static constexpr int NR = (P + 1) * (P + 1);
+  static constexpr int KPAD = (NR + 3) & ~3;
+  static constexpr int NKS = KPAD / 4;
+  static constexpr int NRPAD = (NR + 15) & ~15;
+  static constexpr int NMT = NRPAD / 8;
+  static constexpr int NMMA = NMT / 2;
+  static constexpr int S = ct_xstride(KPAD);
+  static constexpr int NC = 2 * S * 64 * 8 > 140 * 1024 ? 32 : 64;
+  static constexpr int Q = (KPAD + 31) / 32;
+};
+
+template <int NT, int S, int NKS>
+__device__ __forceinline__ void gemm_ct(double (&c)[2][8][2], const double* __restrict__ A0,
+                                        const double* __restrict__ xc, int lane) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+  const double* A1 = A0 + NKS * 32;
+  constexpr int D = 4;
+  double ra0[D], ra1[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    ra0[d] = d < NKS ? __ldg(A0 + d * 32) : 0.0;
+    ra1[d] = d < NKS ? __ldg(A1 + d * 32) : 0.0;
+  }
+  const double* bx = xc + (lane >> 2) * S + (lane & 3);
+#pragma unroll
+  for (int ks = 0; ks < NKS; ++ks) {
+    const double a0 = ra0[ks % D], a1 = ra1[ks % D];
+    if (ks + D < NKS) {
+      ra0[ks % D] = __ldg(A0 + (ks + D) * 32);
+      ra1[ks % D] = __ldg(A1 + (ks + D) * 32);
+    }
+    double bv[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) bv[j] = bx[j * 8 * S + 4 * ks];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      dmma884(c[0][j][0], c[0][j][1], a0, bv[j]);
+      dmma884(c[1][j][0], c[1][j][1], a1, bv[j]);
+    }
+  }
+}
+
+template <int S, int NKS>
+__device__ __forceinline__ void gemm_ct_dispatch(int nta, double (&c)[2][8][2], const double* A0, const double* xc,
+                                                 int lane) {
+  switch (nta) {
+    case 1: gemm_ct<1, S, NKS>(c, A0, xc, lane); break;
+    case 2: gemm_ct<2, S, NKS>(c, A0, xc, lane); break;
+    case 3: gemm_ct<3, S, NKS>(c, A0, xc, lane); break;
+    case 4: gemm_ct<4, S, NKS>(c, A0, xc, lane); break;
+    case 5: gemm_ct<5, S, NKS>(c, A0, xc, lane); break;
+    case 6: gemm_ct<6, S, NKS>(c, A0, xc, lane); break;
+    case 7: gemm_ct<7, S, NKS>(c, A0, xc, lane); break;
+    default: gemm_ct<8, S, NKS>(c, A0, xc, lane); break;
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(512, 1) m2l_ws_ct_kernel(const M2LArgs a, int nhelp) {
+  using G = Geo<P>;
+  constexpr int NR = G::NR, NC = G::NC, S = G::S;
+  extern __shared__ double sm[];
+  const Smem m = carve(sm, a);
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;
+  constexpr int nmma_t = 32 * G::NMMA;
+  const int nhelp_t = 32 * nhelp, nall = nmma_t + nhelp_t;
+  init_smem(a, m, tid, nthr);
+  const int c_first = a.tile_chunk[tile], c_last = a.tile_chunk[tile + 1];
+  __syncthreads();
+  if (warp >= G::NMMA) {
+    const int h = tid - nmma_t, hw = warp - G::NMMA;
+    auto prep = [&](int ch, int b) {
+      load_meta_dev(a, ch, m.meta + b * NC, m.srcs + b * NC, m.sslot + b * NC, m.sbeg + b * (NC + 1), h, nhelp_t);
+      named_sync(6, nhelp_t);
+      gather_cols<4, G::Q>(b ? m.x1 : m.x0, a.chunk_begin[ch + 1] - a.chunk_begin[ch], m.meta + b * NC,
+                           m.srcs + b * NC, m.sym, a.Mt, NR, G::KPAD, S, hw, nhelp, lane);
+    };
+    if (c_first < c_last) {
+      prep(c_first, 0);
+      named_arrive(1, nall);
+    }
+    for (int ch = c_first; ch < c_last; ++ch) {
+      const int i = ch - c_first, b = i & 1, nb = b ^ 1;
+      if (ch + 1 < c_last) {
+        prep(ch + 1, nb);
+        named_arrive(1 + nb, nall);
+      }
+      named_sync(3 + b, nall);
+      accumulate_chunk(m, b ? m.x1 : m.x0, S, NR, a.chunk_seg[ch + 1] - a.chunk_seg[ch], m.meta + b * NC,
+                       m.sbeg + b * (NC + 1), m.sslot + b * NC, h, nhelp_t);
+      named_sync(6, nhelp_t);
+    }
+  } else {
+    for (int ch = c_first; ch < c_last; ++ch) {
+      const int i = ch - c_first, b = i & 1;
+      named_sync(1 + b, nall);
+      double* xc = b ? m.x1 : m.x0;
+      const int cls = a.chunk_class[ch];
+      const int nta = (a.chunk_begin[ch + 1] - a.chunk_begin[ch] + 7) >> 3;
+      double c[2][8][2];
+      const double* A0 = a.ops + (((int64_t)cls * G::NMT + 2 * warp) * G::NKS) * 32 + lane;
+      gemm_ct_dispatch<S, G::NKS>(nta, c, A0, xc, lane);
+      named_sync(5, nmma_t);
+      stage_y(c, xc, S, NR, nta, warp, lane);
+      named_arrive(3 + b, nall);
+    }
+  }
+  __syncthreads();
+  writeback(a, m.acc, m.dec, tile, tid, nthr);
+}
+
+// segment flags: a new slot segment starts at a chunk start or where the slot changes
+__global__ void seg_flag_kernel(const int32_t* __restrict__ col_meta, const int32_t* __restrict__ cflag, int64_t n,
+                                int32_t* __restrict__ sflag) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) sflag[i] = (cflag[i] || (col_meta[i] & 0xff) != (col_meta[i - 1] & 0xff)) ? 1 : 0;
+}
+
+__global__ void seg_emit_kernel(const int32_t* __restrict__ sflag, const int64_t* __restrict__ soff,
+                                const int32_t* __restrict__ cflag, const int64_t* __restrict__ coff, int64_t n,
+                                int32_t* __restrict__ seg_begin, int32_t* __restrict__ chunk_seg) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (sflag[i]) seg_begin[soff[i]] = (int32_t)i;
+  if (cflag[i]) chunk_seg[coff[i]] = (int32_t)soff[i];
+}
+
 }  // namespace
+
+size_t m2l_smem_bytes(const M2LDmma& D) {
+  return ((size_t)D.T * D.NR + 2 * (size_t)D.ystride * D.NC) * sizeof(double) +
+         (8 * D.NC + 2 + 35 * D.NR) * sizeof(int32_t);
+}
 
 void m2l_dmma_setup(fmm_plan_s& P) {
   cudaStream_t s = P.stream;
@@ -468,11 +849,14 @@ void m2l_dmma_setup(fmm_plan_s& P) {
   D.Kpad = (D.NR + 3) / 4 * 4;
   D.nks = D.Kpad / 4;
   D.NC = kNC;
+  D.ystride = D.Kpad;  // column stride S of X[col][k] / Y[col][row]: S >= Kpad, S % 16 == 4
+  while (D.ystride % 16 != 4) ++D.ystride;
+  if (2 * (size_t)D.ystride * D.NC * sizeof(double) > 140 * 1024) D.NC = kNC / 2;  // large p: 32-column chunks
   D.T = 64;
-  while (D.T > 16 && ((size_t)D.T * D.NR + (size_t)std::max(D.Kpad * D.NC, D.NC * (D.NRpad + 2))) * 8 + 8 * D.NC +
-                             132 * D.NR > 200 * 1024)
-    D.T /= 2;
-  D.ystride = D.NRpad + 2;
+  while (D.T > 8 && m2l_smem_bytes(D) > 220 * 1024) D.T /= 2;
+  // warp-specialised kernel: nmt/2 MMA warps + ceil(NR/32) helper warps, <= 512 threads
+  D.nhelp = std::min(2 * ((D.NR + 31) / 32), 16 - D.nmt / 2);
+  D.use_ws = D.nhelp >= 1 && D.NR > 32 && D.Kpad <= 256 && getenv("FMM_M2L_NO_WS") == nullptr;
   int64_t n = P.m2l.n;
   D.npairs = 0;
   D.ntiles = 0;
@@ -573,6 +957,25 @@ void m2l_dmma_setup(fmm_plan_s& P) {
   FMM_LAUNCHED("chunk_emit_kernel");
   const int32_t nn = (int32_t)n;
   FMM_CUDA(cudaMemcpyAsync(D.chunk_begin.ptr + D.nchunks, &nn, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  // slot segments (runs of equal target slot inside a chunk) for the accumulate pass
+  {
+    DevBuf<int32_t> sflag;
+    DevBuf<int64_t> soff;
+    sflag.alloc(n);
+    soff.alloc(n);
+    seg_flag_kernel<<<cdiv(n, 256), 256, 0, s>>>(D.col_meta, cflag, n, sflag);
+    FMM_LAUNCHED("seg_flag_kernel");
+    D.nseg = scan_counts_total(sflag, soff, n, s);
+    D.seg_begin.alloc(D.nseg + 1);
+    D.chunk_seg.alloc(D.nchunks + 1);
+    seg_emit_kernel<<<cdiv(n, 256), 256, 0, s>>>(sflag, soff, cflag, coff, n, D.seg_begin, D.chunk_seg);
+    FMM_LAUNCHED("seg_emit_kernel");
+    const int32_t ns32 = (int32_t)D.nseg;
+    FMM_CUDA(cudaMemcpyAsync(D.seg_begin.ptr + D.nseg, &nn, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    FMM_CUDA(cudaMemcpyAsync(D.chunk_seg.ptr + D.nchunks, &ns32, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+  }
+  D.Mt.alloc(C.n * D.Kpad);
   D.tile_chunk.alloc(D.ntiles + 1);
   tile_chunk_kernel<<<cdiv(D.nchunks + 1, 256), 256, 0, s>>>(ctile, D.nchunks, D.ntiles, D.tile_chunk);
   FMM_LAUNCHED("tile_chunk_kernel");
@@ -583,18 +986,24 @@ void m2l_dmma_pass(fmm_plan_s& P) {
   M2LDmma& D = P.m2l_dmma;
   FMM_CUDA(cudaMemsetAsync(P.L.ptr, 0, sizeof(double2) * P.L.count, P.stream));
   if (D.ntiles == 0) return;
+  const int64_t ne = P.cells.n * D.Kpad;
+  mtilde_kernel<<<cdiv(ne, 256), 256, 0, P.stream>>>(P.M, P.cells.level, D.hpow, P.cells.n, P.p, P.nc, D.NR, D.Kpad,
+                                                     D.Mt);
+  FMM_LAUNCHED("mtilde_kernel");
   M2LArgs a;
   a.ops = D.ops;
   a.col_src = D.col_src;
   a.col_meta = D.col_meta;
   a.chunk_begin = D.chunk_begin;
   a.chunk_class = D.chunk_class;
+  a.chunk_seg = D.chunk_seg;
+  a.seg_begin = D.seg_begin;
   a.tile_chunk = D.tile_chunk;
   a.tile_cells = D.tile_cells;
   a.symtab = D.symtab;
   a.hpow = D.hpow;
   a.level = P.cells.level;
-  a.M = P.M;
+  a.Mt = D.Mt;
   a.L = P.L;
   a.p = P.p;
   a.nc = P.nc;
@@ -606,14 +1015,47 @@ void m2l_dmma_pass(fmm_plan_s& P) {
   a.T = D.T;
   a.NC = D.NC;
   a.ystride = D.ystride;
-  const size_t sh = ((size_t)D.T * D.NR + (size_t)std::max(D.Kpad * D.NC, D.NC * D.ystride)) * sizeof(double) +
-                    (2 * D.NC + 33 * D.NR) * sizeof(int32_t);
-  static size_t configured = 0;
-  if (sh > 48 * 1024 && sh > configured) {
-    FMM_CUDA(cudaFuncSetAttribute(m2l_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    configured = sh;
+  const size_t sh = m2l_smem_bytes(D);
+  const int threads = 32 * (D.nmt / 2);
+  static size_t configured[2] = {0, 0};  // dynamic-smem opt-in per kernel
+  const int nmma = D.nmt / 2, nhelp = D.nhelp;
+  static size_t configured_ct[16] = {0};
+  if (D.use_ws && P.p >= 5 && P.p <= 14 && getenv("FMM_M2L_NO_CT") == nullptr) {
+    void (*k)(const M2LArgs, int) = nullptr;
+    switch (P.p) {
+      case 5: k = m2l_ws_ct_kernel<5>; break;
+      case 6: k = m2l_ws_ct_kernel<6>; break;
+      case 7: k = m2l_ws_ct_kernel<7>; break;
+      case 8: k = m2l_ws_ct_kernel<8>; break;
+      case 9: k = m2l_ws_ct_kernel<9>; break;
+      case 10: k = m2l_ws_ct_kernel<10>; break;
+      case 11: k = m2l_ws_ct_kernel<11>; break;
+      case 12: k = m2l_ws_ct_kernel<12>; break;
+      case 13: k = m2l_ws_ct_kernel<13>; break;
+      default: k = m2l_ws_ct_kernel<14>; break;
+    }
+    if (sh > 48 * 1024 && sh > configured_ct[P.p]) {
+      FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+      configured_ct[P.p] = sh;
+    }
+    k<<<(unsigned)D.ntiles, 32 * (nmma + nhelp), sh, P.stream>>>(a, nhelp);
+    FMM_LAUNCHED("m2l_ws_ct_kernel");
+    return;
   }
-  const int threads = 32 * (D.nmt / 2 + (D.nmt & 1));
+  if (D.use_ws) {
+    if (sh > 48 * 1024 && sh > configured[1]) {
+      FMM_CUDA(cudaFuncSetAttribute(m2l_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+      configured[1] = sh;
+    }
+    const char* dbg = getenv("FMM_M2L_DEBUG");  // timing experiments only (skips work: wrong results)
+    m2l_ws_kernel<<<(unsigned)D.ntiles, 32 * (nmma + nhelp), sh, P.stream>>>(a, nmma, nhelp, dbg ? atoi(dbg) : 0);
+    FMM_LAUNCHED("m2l_ws_kernel");
+    return;
+  }
+  if (sh > 48 * 1024 && sh > configured[0]) {
+    FMM_CUDA(cudaFuncSetAttribute(m2l_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+    configured[0] = sh;
+  }
   m2l_dmma_kernel<<<(unsigned)D.ntiles, threads, sh, P.stream>>>(a);
   FMM_LAUNCHED("m2l_dmma_kernel");
 }

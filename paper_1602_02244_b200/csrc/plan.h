@@ -70,7 +70,12 @@ struct PairList {
 // M2L v2 state (m2l_dmma.cu): canonical operator classes, tiles, chunks.
 struct M2LDmma {
   int NR = 0, NRpad = 0, nmt = 0, Kpad = 0, nks = 0, NC = 0, T = 0, ystride = 0;
-  int64_t nclass = 0, ntiles = 0, nchunks = 0, npairs = 0;
+  bool use_ws = false;  // warp-specialised DMMA kernel
+  int nhelp = 0;        // its helper warps
+  int64_t nclass = 0, ntiles = 0, nchunks = 0, npairs = 0, nseg = 0;
+  DevBuf<int32_t> chunk_seg;   // [nchunks + 1] first slot segment of each chunk
+  DevBuf<int32_t> seg_begin;   // [nseg + 1] first column of each slot segment
+  DevBuf<double> Mt;           // [ncells][Kpad] scaled real-form multipoles (per matvec)
   DevBuf<double> ops;          // [nclass][nmt][nks][32] A fragments
   DevBuf<int32_t> col_src;     // [npairs] source cell per GEMM column
   DevBuf<int32_t> col_meta;    // [npairs] slot | g << 8
@@ -82,7 +87,8 @@ struct M2LDmma {
   DevBuf<double> hpow;         // [22][p + 2]
   int64_t bytes() const {
     return ops.bytes() + col_src.bytes() + col_meta.bytes() + chunk_begin.bytes() + chunk_class.bytes() +
-           tile_chunk.bytes() + tile_cells.bytes() + symtab.bytes() + hpow.bytes();
+           tile_chunk.bytes() + tile_cells.bytes() + symtab.bytes() + hpow.bytes() + chunk_seg.bytes() +
+           seg_begin.bytes() + Mt.bytes();
   }
 };
 

@@ -136,7 +136,10 @@ void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
     FMM_CUDA(cudaMemsetAsync(phi, 0, sizeof(double) * P.n, P.stream));
     if (grad) FMM_CUDA(cudaMemsetAsync(grad, 0, sizeof(double) * 3 * P.n, P.stream));
   }
-  fmm::near_pass(P, q, phi, grad);
+  if (P.near_variant == 2)
+    fmm::near_pass_warp(P, phi, grad);
+  else
+    fmm::near_pass(P, q, phi, grad);
   T.mark(4);
   if (T.on) {
     FMM_CUDA(cudaEventSynchronize(P.ev[4]));
@@ -211,6 +214,8 @@ fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncr
     choose_own_range(*P);
     const char* v = getenv("FMM_M2L_VARIANT");
     if (v && v[0] == '1') P->m2l_variant = 1;
+    const char* nv = getenv("FMM_NEAR_VARIANT");
+    if (nv && nv[0] == '1') P->near_variant = 1;
     const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // test hook: export M2L-only local expansions
     P->debug_skip_l2l = dbg && dbg[0] == '1';
     if (P->m2l_variant == 2) fmm::m2l_dmma_setup(*P);

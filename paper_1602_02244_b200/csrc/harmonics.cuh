@@ -62,4 +62,59 @@ __device__ __forceinline__ void decode_jk(int t, int& j, int& k) {
   k = t - cidx(j, 0);
 }
 
+// L2P (+grad) for one target with the regular harmonics generated on the fly
+// (two-term column recurrence, O(1) registers), using the m >= 0 symmetry:
+//   phi   = sum_n sum_{m>=0} w_m Re(L_n^m conj R_n^m),  w_0 = 1, w_{m>0} = 2
+//   L'_0  = sum_{n<p} sum_{m>=0} w_m Re(L_{n+1}^m conj R_n^m)
+//   L'_1  = sum_{n<p} sum_{m>=0} [L_{n+1}^{m+1} conj R_n^m - [m>0] conj(L_{n+1}^{m-1}) R_n^m]
+//   grad  = (-Re L'_1, -Im L'_1, L'_0)
+// (the same quantities as the oracle's full-m sums, regrouped).
+template <bool kGrad>
+__device__ __forceinline__ void l2p_eval(const double2* __restrict__ Lc, int p, double x, double y, double z,
+                                         double& phi, double3& g) {
+  const double r2 = x * x + y * y + z * z;
+  double2 diag = make_double2(1.0, 0.0);
+  double f = 0.0, g0 = 0.0;
+  double2 g1 = make_double2(0.0, 0.0);
+  for (int m = 0; m <= p; ++m) {
+    if (m > 0) {
+      const double s = -0.5 / m;
+      diag = cmul(diag, make_double2(s * x, s * y));
+    }
+    const double w = m == 0 ? 1.0 : 2.0;
+    double2 a = make_double2(0, 0), b = diag;  // R_{n-1}^m, R_n^m
+    for (int n = m; n <= p; ++n) {
+      if (n == m + 1) {
+        a = b;
+        b = cscale(diag, z);
+      } else if (n > m + 1) {
+        const double inv = 1.0 / ((double)(n + m) * (double)(n - m));
+        double2 c = make_double2(((2 * n - 1) * z * b.x - r2 * a.x) * inv, ((2 * n - 1) * z * b.y - r2 * a.y) * inv);
+        a = b;
+        b = c;
+      }
+      const double2 l = Lc[cidx(n, m)];
+      f += w * (l.x * b.x + l.y * b.y);
+      if (kGrad && n < p) {
+        const double2 l0 = Lc[cidx(n + 1, m)];
+        g0 += w * (l0.x * b.x + l0.y * b.y);
+        const double2 lp = Lc[cidx(n + 1, m + 1)];  // L_{n+1}^{m+1} conj R
+        g1.x += lp.x * b.x + lp.y * b.y;
+        g1.y += lp.y * b.x - lp.x * b.y;
+        if (m > 0) {  // - conj(L_{n+1}^{m-1}) R
+          const double2 lm = Lc[cidx(n + 1, m - 1)];
+          g1.x -= lm.x * b.x + lm.y * b.y;
+          g1.y -= lm.x * b.y - lm.y * b.x;
+        }
+      }
+    }
+  }
+  phi += f;
+  if (kGrad) {
+    g.x -= g1.x;
+    g.y -= g1.y;
+    g.z += g0;
+  }
+}
+
 }  // namespace fmm

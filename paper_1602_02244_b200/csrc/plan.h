@@ -128,6 +128,7 @@ struct fmm_plan_s {
   int64_t n_p2p_interactions = 0;
   fmm::M2LDmma m2l_dmma;
   int m2l_variant = 2;  // 1 = matrix-free O(p^4) per pair (v1), 2 = DMMA operator classes (v2)
+  int near_variant = 2; // 1 = block per leaf, thread per target (v1), 2 = warp per leaf (v2)
 
   // this rank's targets (Morton range of sorted positions) and its leaves
   int64_t own_begin = 0, own_end = 0;
@@ -158,6 +159,7 @@ void m2l_dmma_setup(fmm_plan_s& P);
 void m2l_dmma_pass(fmm_plan_s& P);
 void downward(fmm_plan_s& P);
 void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
+void near_pass_warp(fmm_plan_s& P, double* phi, double* grad);
 void gather_charges(fmm_plan_s& P, const double* q);
 void launch_direct(const double* src, const double* q, int64_t ns, const double* tgt, int64_t nt,
                    double* phi, double* grad, cudaStream_t s);

@@ -253,3 +253,24 @@ def test_m2l_variants(torch_cuda, monkeypatch, variant, dist, n, p, ncrit, theta
     _, phi, g = gpu_fmm(torch, x, q, p, ncrit, theta, grad=True)
     po, go = O.fmm(x, q, p, ncrit, theta, grad=True, nthreads=O.default_threads())
     assert O.rel_l2(phi, po) <= TOL and O.rel_l2(g, go) <= TOL
+
+
+@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("dist,n,p,ncrit,theta,grad", [("plummer", 20000, 4, 64, 0.5, True),
+                                                       ("cube", 20000, 4, 200, 0.4, False),
+                                                       ("sphere", 20000, 4, 7, 0.4, True),
+                                                       ("cube", 3000, 2, 16, 1e-6, True)])
+def test_near_variants(torch_cuda, monkeypatch, variant, dist, n, p, ncrit, theta, grad):
+    """Near-field kernels (v1 block per leaf; v2 warp per leaf with shared-memory staging,
+    lanes-per-target splitting and rsqrt seed + third-order correction) match the oracle;
+    ncrit 200 exercises leaves with more than 128 sources (chunked staging) and 64+ targets."""
+    monkeypatch.setenv("FMM_NEAR_VARIANT", variant)
+    torch = torch_cuda
+    x, q = F.make(dist, n)
+    _, phi, g = gpu_fmm(torch, x, q, p, ncrit, theta, grad=grad)
+    res = O.fmm(x, q, p, ncrit, theta, grad=grad, nthreads=O.default_threads())
+    po, go = res if grad else (res, None)
+    tol = 1e-14 if theta < 1e-3 else TOL  # all-P2P case: only rounding differs
+    assert O.rel_l2(phi, po) <= tol
+    if grad:
+        assert O.rel_l2(g, go) <= tol

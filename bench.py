@@ -356,8 +356,15 @@ def main():
     else:
         dom, dflops, dms = "near (L2P+P2P)", near_flops, near_ms
     achieved = dflops / (dms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(dom, {}).get("bytes")
+    except (OSError, ValueError):
+        pass
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
-                "frac": achieved / nominal, "traffic": None,
+                "frac": achieved / nominal, "traffic": traffic,
+                "traffic_source": "profiles/traffic.json (ncu --set full, DRAM read+write bytes per launch)",
                 "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz (DESIGN.md §2)",
                 "measured_fp64_probe": probe,
                 "stages_ms": {"upward": up_ms, "m2l": m2l_ms, "downward": down_ms, "near": near_ms},

@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-]
+] + os.environ.get("FMM_NVCC_EXTRA", "").split()  # experiments only (e.g. -DFMM_NEAR_MINB=4)
 
 
 def sources():

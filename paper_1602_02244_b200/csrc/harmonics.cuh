@@ -6,6 +6,20 @@
 
 namespace fmm {
 
+// 1 / ((n + m)(n - m)) for the regular-harmonic column recurrence (n >= m + 2), in
+// constant memory: the L2P loop indices are warp-uniform, so reads are broadcasts and
+// the per-coefficient FP64 division disappears.
+struct InvNM {
+  double v[(kMaxP + 1) * (kMaxP + 1)];
+};
+constexpr InvNM make_inv_nm() {
+  InvNM t{};
+  for (int n = 0; n <= kMaxP; ++n)
+    for (int m = 0; m <= kMaxP; ++m) t.v[n * (kMaxP + 1) + m] = (n > m) ? 1.0 / ((double)(n + m) * (double)(n - m)) : 0.0;
+  return t;
+}
+static __constant__ InvNM c_inv_nm = make_inv_nm();
+
 // Regular harmonics R_n^m(x,y,z), n <= p, written by ONE thread into R.
 __device__ inline void regular_harmonics(double x, double y, double z, int p, double2* R) {
   const double r2 = x * x + y * y + z * z;
@@ -88,7 +102,7 @@ __device__ __forceinline__ void l2p_eval(const double2* __restrict__ Lc, int p, 
         a = b;
         b = cscale(diag, z);
       } else if (n > m + 1) {
-        const double inv = 1.0 / ((double)(n + m) * (double)(n - m));
+        const double inv = c_inv_nm.v[n * (kMaxP + 1) + m];
         double2 c = make_double2(((2 * n - 1) * z * b.x - r2 * a.x) * inv, ((2 * n - 1) * z * b.y - r2 * a.y) * inv);
         a = b;
         b = c;

@@ -1,19 +1,25 @@
 // near_warp.cu — S11 L2P(+grad), S12 P2P and S13 un-permute, v2: one WARP per target
 // leaf (the direct operator is the dense diagonal block).
 //
-//  * targets: a leaf with nt <= 32 targets uses G = 32 / pow2ceil(nt) (<= 8) lanes per
-//    target, each summing every G-th source, reduced with shuffles; larger leaves run
-//    in groups of 64 targets with 2 targets per lane (register blocking);
-//  * sources: the source leaves of the P2P list are Morton-contiguous runs of double4
-//    (x, y, z, q); each is staged into the warp's shared-memory buffer with cp.async
-//    (16 B copies), double-buffered so the next leaf streams in during compute;
-//    all lanes of a target group read the same source -> shared-memory broadcast;
+//  * lane layout per leaf: nt targets are covered by (32 / G) target groups of G lanes,
+//    each lane holding TPL targets in registers (G in {1,2,4,8}, TPL <= 4), chosen per
+//    leaf to minimise the idle slots (32 / G) * TPL - nt; the G lanes of a group split
+//    the sources (every G-th one) and are reduced with a butterfly at the end, so every
+//    lane of the group holds the full sums and the L2P evaluations are spread over them;
+//  * sources: the leaf's P2P source leaves are Morton-contiguous runs of double4
+//    (x, y, z, q); consecutive list entries are packed into staging units of up to
+//    kBuf particles (the self leaf always alone, it alone needs the r^2 == 0 test),
+//    copied into the warp's shared-memory buffer with cp.async (16 B pieces) and
+//    double-buffered so the next unit streams in during compute; the lanes of a
+//    group read distinct sources, the groups the same ones (shared-memory broadcast);
 //  * 1/r: rsqrt.approx.f64 seed (MUFU) + one third-order correction
 //    y1 = y0 (1 + e/2 + 3e^2/8), e = 1 - r^2 y0^2: relative error O(e^3) << 2^-53,
 //    5 FP64 ops; r^2 == 0 (self term, coincident points) is tested only in the
-//    self-leaf loop, since equal coordinates imply equal keys and the same leaf
+//    self-leaf unit, since equal coordinates imply equal keys and the same leaf
 //    (R2, R11).
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "harmonics.cuh"
 #include "plan.h"
@@ -23,6 +29,16 @@ namespace {
 
 constexpr int kWarps = 4;   // warps (target leaves) per CTA
 constexpr int kBuf = 128;   // source particles per staging buffer
+constexpr int kMaxTPL = 4;  // targets per lane (measured: 8 is slower, register pressure)
+template <bool kGrad>
+constexpr int max_tpl() { return kMaxTPL; }
+#ifndef FMM_NEAR_MINB
+#define FMM_NEAR_MINB 4  // CTAs per SM for the phi-only kernel (122 registers, no spills)
+#endif
+#ifndef FMM_NEAR_UNROLL
+#define FMM_NEAR_UNROLL 2
+#endif
+constexpr int kUnroll = FMM_NEAR_UNROLL;
 
 __device__ __forceinline__ double rsqrt_fp64(double x) {
   double y;
@@ -42,15 +58,17 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// a staging unit: up to kBuf particles of source leaf q (chunk `off` of it)
+// A staging unit: list entries [qa, qb) from particle `off` of entry qa (off > 0 only
+// for a leaf larger than kBuf, which is then a unit of its own), n particles in total.
 struct Unit {
-  int q, off;
+  int qa, qb, off, n;
+  bool self;
 };
 
 template <bool kGrad, bool kCheck, int TPL>
-__device__ __forceinline__ void interact(const double4* __restrict__ sb, int ns, int sg, int G, const double3 (&xi)[TPL],
-                                         double (&f)[TPL], double3 (&g)[TPL]) {
-#pragma unroll 4
+__device__ __forceinline__ void interact(const double4* __restrict__ sb, int ns, int sg, int G,
+                                         const double3 (&xi)[TPL], double (&f)[TPL], double3 (&g)[TPL]) {
+#pragma unroll kUnroll
   for (int j = sg; j < ns; j += G) {
     const double4 s = sb[j];
 #pragma unroll
@@ -73,74 +91,91 @@ __device__ __forceinline__ void interact(const double4* __restrict__ sb, int ns,
   }
 }
 
+struct NearArgs {
+  const int32_t* cbeg;
+  const int32_t* cend;
+  const double4* center;
+  const double4* pos;
+  const double2* L;
+  const int32_t* off;
+  const int32_t* src;
+  const uint32_t* perm;
+  int p, nc;
+  double s_phi, s_grad;
+  double* phi_out;
+  double* grad_out;
+  int max_tpl, max_g;  // layout limits (tuning; defaults max_tpl<kGrad>(), 8)
+};
+
+// Targets [t0, t0 + cnt) of `leaf` as (32 / G) groups x TPL targets per lane.
 template <bool kGrad, int TPL>
-__device__ void process_group(int leaf, int t0, int cnt, int lane, double4 (*buf)[kBuf],
-                              const int32_t* __restrict__ cbeg, const int32_t* __restrict__ cend,
-                              const double4* __restrict__ center, const double4* __restrict__ pos,
-                              const double2* __restrict__ L, const int32_t* __restrict__ off,
-                              const int32_t* __restrict__ src, const uint32_t* __restrict__ perm, int p, int nc,
-                              double s_phi, double s_grad, double* __restrict__ phi_out,
-                              double* __restrict__ grad_out) {
-  // lanes per target (TPL == 1 only): largest power of two with G * cnt <= 32, at most 8
-  int G = 1;
-  if (TPL == 1) {
-    while (G < 8 && 2 * G * cnt <= 32) G *= 2;
-  }
-  const int tl = lane / G, sg = lane - tl * G;
+__device__ void process_group(const NearArgs& a, int leaf, int t0, int cnt, int G, int lane, double4 (*buf)[kBuf]) {
+  const int tl = lane / G, sg = lane - tl * G, ngrp = 32 / G;
   double3 xi[TPL];
   double f[TPL];
   double3 g[TPL];
-  bool act[TPL];
 #pragma unroll
   for (int k = 0; k < TPL; ++k) {
-    const int t = tl + 32 * k;
-    act[k] = t < cnt;
-    const double4 v = act[k] ? pos[t0 + t] : make_double4(0, 0, 0, 0);
+    const int t = tl + ngrp * k;
+    const double4 v = t < cnt ? a.pos[t0 + t] : make_double4(0, 0, 0, 0);
     xi[k] = make_double3(v.x, v.y, v.z);
     f[k] = 0.0;
     g[k] = make_double3(0, 0, 0);
   }
-  const int q0 = off[leaf], q1 = off[leaf + 1];
-  // staging pipeline over units (source leaf q, chunk offset)
-  auto stage = [&](Unit u, int b) {
-    const int sl = src[u.q];
-    const int sb = cbeg[sl] + u.off;
-    const int n = min(kBuf, cend[sl] - sb);
-    const double* gsrc = (const double*)(pos + sb);
+  const int q1 = a.off[leaf + 1];
+  // Build and issue (cp.async) the unit starting at (qa, off) into buffer b.
+  auto stage = [&](int qa, int off, int b) -> Unit {
+    Unit u{qa, qa, off, 0, false};
     double* dst = (double*)buf[b];
-    for (int h = lane; h < 2 * n; h += 32) cp_async16(dst + 2 * h, gsrc + 2 * h);
+    for (int q = qa; q < q1; ++q) {
+      const int sl = a.src[q];
+      const int sb = a.cbeg[sl] + (q == qa ? off : 0);
+      const int sz = a.cend[sl] - sb;
+      const bool self = sl == leaf;
+      if (q > qa && (self || sz > kBuf - u.n)) break;  // the unit is full / the self leaf goes alone
+      const int n = min(kBuf - u.n, sz);
+      const double* gsrc = (const double*)(a.pos + sb);
+      for (int h = lane; h < 2 * n; h += 32) cp_async16(dst + 4 * u.n + 2 * h, gsrc + 2 * h);
+      u.n += n;
+      u.qb = q + 1;
+      u.self = self;
+      if (self || n < sz) {  // self leaf alone; an oversized leaf continues in the next unit
+        if (n < sz) u.qb = q;
+        break;
+      }
+    }
     cp_commit();
+    return u;
   };
-  auto next = [&](Unit u) {
-    const int sl = src[u.q];
-    if (u.off + kBuf < cend[sl] - cbeg[sl]) return Unit{u.q, u.off + kBuf};
-    return Unit{u.q + 1, 0};
+  auto next_of = [&](const Unit& u) -> int2 {  // (qa, off) after u
+    if (u.qb == u.qa) return make_int2(u.qa, u.off + u.n);  // partial oversized leaf
+    return make_int2(u.qb, 0);
   };
-  if (q0 < q1) {
-    Unit u{q0, 0};
-    stage(u, 0);
-    int b = 0;
-    while (u.q < q1) {
-      const Unit un = next(u);
-      if (un.q < q1) {
-        stage(un, b ^ 1);
+  int qa = a.off[leaf], off = 0, b = 0;
+  if (qa < q1) {
+    Unit u = stage(qa, off, 0);
+    while (true) {
+      const int2 nx = next_of(u);
+      Unit un{0, 0, 0, 0, false};
+      const bool more = nx.x < q1;
+      if (more) {
+        un = stage(nx.x, nx.y, b ^ 1);
         cp_wait<1>();
       } else {
         cp_wait<0>();
       }
       __syncwarp();
-      const int sl = src[u.q];
-      const int ns = min(kBuf, cend[sl] - cbeg[sl] - u.off);
-      if (sl == leaf)
-        interact<kGrad, true, TPL>(buf[b], ns, sg, G, xi, f, g);
+      if (u.self)
+        interact<kGrad, true, TPL>(buf[b], u.n, sg, G, xi, f, g);
       else
-        interact<kGrad, false, TPL>(buf[b], ns, sg, G, xi, f, g);
-      __syncwarp();  // buffer b is rewritten two units later
+        interact<kGrad, false, TPL>(buf[b], u.n, sg, G, xi, f, g);
+      __syncwarp();  // buffer b is rewritten by the unit after next
+      if (!more) break;
       u = un;
       b ^= 1;
     }
   }
-  // reduce the G partial sums of each target
+  // butterfly over the G lanes of each group: every lane ends with the group's sums
   for (int o = 1; o < G; o <<= 1) {
 #pragma unroll
     for (int k = 0; k < TPL; ++k) {
@@ -152,43 +187,80 @@ __device__ void process_group(int leaf, int t0, int cnt, int lane, double4 (*buf
       }
     }
   }
-  if (sg != 0) return;
-  const double4 c = center[leaf];
-  const double2* Lc = L + (int64_t)leaf * nc;
+  // L2P + store: lane sg of a group evaluates its targets k = sg, sg + G, ...
+  const double4 c = a.center[leaf];
+  const double2* Lc = a.L + (int64_t)leaf * a.nc;
+  for (int k0 = 0; k0 < TPL; k0 += G) {
+    const int kk = k0 + sg;
+    double3 x = make_double3(0, 0, 0), gg = make_double3(0, 0, 0);
+    double ff = 0.0;
 #pragma unroll
-  for (int k = 0; k < TPL; ++k) {
-    if (!act[k]) continue;
-    l2p_eval<kGrad>(Lc, p, xi[k].x - c.x, xi[k].y - c.y, xi[k].z - c.z, f[k], g[k]);
-    const int64_t o = perm[t0 + tl + 32 * k];
-    phi_out[o] = f[k] * s_phi;
-    if (kGrad) {
-      grad_out[3 * o] = g[k].x * s_grad;
-      grad_out[3 * o + 1] = g[k].y * s_grad;
-      grad_out[3 * o + 2] = g[k].z * s_grad;
+    for (int k = 0; k < TPL; ++k)
+      if (k == kk) {
+        x = xi[k];
+        ff = f[k];
+        gg = g[k];
+      }
+    const int t = tl + ngrp * kk;
+    if (kk < TPL && t < cnt) {
+      l2p_eval<kGrad>(Lc, a.p, x.x - c.x, x.y - c.y, x.z - c.z, ff, gg);
+      const int64_t o = a.perm[t0 + t];
+      a.phi_out[o] = ff * a.s_phi;
+      if (kGrad) {
+        a.grad_out[3 * o] = gg.x * a.s_grad;
+        a.grad_out[3 * o + 1] = gg.y * a.s_grad;
+        a.grad_out[3 * o + 2] = gg.z * a.s_grad;
+      }
+    }
+  }
+}
+
+// (G, TPL) minimising the idle slots (32 / G) * TPL - cnt; ties prefer TPL >= G (balanced
+// L2P), then larger TPL (more register reuse of each staged source). TPL == 0: none fits.
+template <bool kGrad>
+__device__ __forceinline__ void choose_layout(int cnt, int maxT, int maxG, int& G, int& TPL) {
+  int best = 1 << 30;
+  G = 1;
+  TPL = 0;
+  for (int g = 8; g >= 1; g >>= 1) {
+    const int per = 32 / g, t = (cnt + per - 1) / per;
+    if (t > maxT || g > maxG) continue;
+    const int key = (per * t) * 4 + (t >= g ? 0 : 2) + (t > TPL ? 0 : 1);
+    if (key < best) {
+      best = key;
+      G = g;
+      TPL = t;
     }
   }
 }
 
 template <bool kGrad>
-__global__ void __launch_bounds__(32 * kWarps) near_warp_kernel(
-    const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ cbeg,
-    const int32_t* __restrict__ cend, const double4* __restrict__ center, const double4* __restrict__ pos,
-    const double2* __restrict__ L, const int32_t* __restrict__ off, const int32_t* __restrict__ src,
-    const uint32_t* __restrict__ perm, int p, int nc, double s_phi, double s_grad, double* __restrict__ phi_out,
-    double* __restrict__ grad_out) {
+__device__ __forceinline__ void dispatch(const NearArgs& a, int leaf, int t0, int cnt, int G, int TPL, int lane,
+                                         double4 (*buf)[kBuf]) {
+  switch (TPL) {
+    case 1: process_group<kGrad, 1>(a, leaf, t0, cnt, G, lane, buf); break;
+    case 2: process_group<kGrad, 2>(a, leaf, t0, cnt, G, lane, buf); break;
+    case 3: process_group<kGrad, 3>(a, leaf, t0, cnt, G, lane, buf); break;
+    case 4: process_group<kGrad, 4>(a, leaf, t0, cnt, G, lane, buf); break;
+  }
+}
+
+template <bool kGrad>
+__global__ void __launch_bounds__(32 * kWarps, kGrad ? 3 : FMM_NEAR_MINB) near_warp_kernel(const int32_t* __restrict__ leaves, int64_t nleaves,
+                                                                const NearArgs a) {
   __shared__ __align__(16) double4 buf[kWarps][2][kBuf];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t li = (int64_t)blockIdx.x * kWarps + warp;
   if (li >= nleaves) return;  // warp-uniform; no block-level barriers below
   const int leaf = leaves[li];
-  const int tb = cbeg[leaf], te = cend[leaf];
-  if (te - tb <= 32) {
-    process_group<kGrad, 1>(leaf, tb, te - tb, lane, buf[warp], cbeg, cend, center, pos, L, off, src, perm, p, nc,
-                            s_phi, s_grad, phi_out, grad_out);
-  } else {
-    for (int t0 = tb; t0 < te; t0 += 64)
-      process_group<kGrad, 2>(leaf, t0, min(64, te - t0), lane, buf[warp], cbeg, cend, center, pos, L, off, src,
-                              perm, p, nc, s_phi, s_grad, phi_out, grad_out);
+  const int tb = a.cbeg[leaf], te = a.cend[leaf];
+  int G, TPL;
+  choose_layout<kGrad>(te - tb, a.max_tpl, a.max_g, G, TPL);
+  if (TPL > 0) {
+    dispatch<kGrad>(a, leaf, tb, te - tb, G, TPL, lane, buf[warp]);
+  } else {  // more than 32 * kMaxTPL targets: groups of 32 * kMaxTPL, one lane per target
+    constexpr int T = max_tpl<kGrad>();
+    for (int t0 = tb; t0 < te; t0 += 32 * T) process_group<kGrad, T>(a, leaf, t0, min(32 * T, te - t0), 1, lane, buf[warp]);
   }
 }
 
@@ -197,17 +269,31 @@ __global__ void __launch_bounds__(32 * kWarps) near_warp_kernel(
 void near_pass_warp(fmm_plan_s& P, double* phi, double* grad) {
   const int64_t nl = P.own_leaf_end - P.own_leaf_begin;
   if (nl <= 0) return;
-  const double s_phi = std::ldexp(1.0, -P.e), s_grad = std::ldexp(1.0, -2 * P.e);
+  NearArgs a;
+  a.cbeg = P.cells.begin;
+  a.cend = P.cells.end;
+  a.center = P.cells.center;
+  a.pos = P.pos;
+  a.L = P.L;
+  a.off = P.p2p.off;
+  a.src = P.p2p.src;
+  a.perm = P.perm;
+  a.p = P.p;
+  a.nc = P.nc;
+  a.s_phi = std::ldexp(1.0, -P.e);
+  a.s_grad = std::ldexp(1.0, -2 * P.e);
+  a.phi_out = phi;
+  a.grad_out = grad;
+  a.max_tpl = grad ? max_tpl<true>() : max_tpl<false>();
+  a.max_g = 8;
+  if (const char* e = getenv("FMM_NEAR_MAXTPL")) a.max_tpl = std::max(1, std::min(a.max_tpl, atoi(e)));
+  if (const char* e = getenv("FMM_NEAR_MAXG")) a.max_g = std::max(1, std::min(8, atoi(e)));
   const int32_t* leaves = P.leaves.ptr + P.own_leaf_begin;
   const unsigned grid = cdiv(nl, kWarps);
   if (grad)
-    near_warp_kernel<true><<<grid, 32 * kWarps, 0, P.stream>>>(leaves, nl, P.cells.begin, P.cells.end,
-                                                               P.cells.center, P.pos, P.L, P.p2p.off, P.p2p.src,
-                                                               P.perm, P.p, P.nc, s_phi, s_grad, phi, grad);
+    near_warp_kernel<true><<<grid, 32 * kWarps, 0, P.stream>>>(leaves, nl, a);
   else
-    near_warp_kernel<false><<<grid, 32 * kWarps, 0, P.stream>>>(leaves, nl, P.cells.begin, P.cells.end,
-                                                                P.cells.center, P.pos, P.L, P.p2p.off, P.p2p.src,
-                                                                P.perm, P.p, P.nc, s_phi, s_grad, phi, grad);
+    near_warp_kernel<false><<<grid, 32 * kWarps, 0, P.stream>>>(leaves, nl, a);
   FMM_LAUNCHED("near_warp_kernel");
 }
 

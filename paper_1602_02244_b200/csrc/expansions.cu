@@ -17,8 +17,10 @@ namespace {
 
 constexpr int kExpThreads = 128;  // >= ncoef(p) for p <= 14; two outputs per thread up to p = 21
 constexpr int kP2MChunk = 32;     // particles whose harmonics are staged per round
+constexpr int kM2MThreads = 256;  // M2M / L2L: items (child, coefficient)
 
-// S7 P2M: M_n^m(c) = sum_i q_i conj R_n^m(x_i - c), one block per leaf.
+// S7 P2M: M_n^m(c) = sum_i q_i conj R_n^m(x_i - c), one block per leaf; the harmonics
+// of a chunk of particles are computed column-parallel (item = (particle, m)).
 __global__ void p2m_kernel(const int32_t* __restrict__ leaves, const int32_t* __restrict__ cbeg,
                            const int32_t* __restrict__ cend, const double4* __restrict__ center,
                            const double4* __restrict__ pos, int p, int nc, double2* __restrict__ M) {
@@ -30,11 +32,15 @@ __global__ void p2m_kernel(const int32_t* __restrict__ leaves, const int32_t* __
   double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
   for (int32_t s0 = b; s0 < e; s0 += kP2MChunk) {
     const int cnt = min(kP2MChunk, e - s0);
-    if (threadIdx.x < cnt) {
-      const double4 x = pos[s0 + threadIdx.x];
-      double2* R = shR + threadIdx.x * nc;
-      regular_harmonics(x.x - c.x, x.y - c.y, x.z - c.z, p, R);
-      for (int t = 0; t < nc; ++t) R[t] = make_double2(x.w * R[t].x, -x.w * R[t].y);
+    for (int it = threadIdx.x; it < cnt * (p + 1); it += blockDim.x) {
+      const int i = it / (p + 1), m = it - i * (p + 1);
+      const double4 x = pos[s0 + i];
+      double2* R = shR + i * nc;
+      regular_column(x.x - c.x, x.y - c.y, x.z - c.z, m, p, R);
+      for (int n = m; n <= p; ++n) {
+        const double2 v = R[cidx(n, m)];
+        R[cidx(n, m)] = make_double2(x.w * v.x, -x.w * v.y);
+      }
     }
     __syncthreads();
     for (int k = 0; k < cnt; ++k) {
@@ -57,35 +63,39 @@ __device__ __forceinline__ double2 m2m_term(const double2* R, const double2* Mc,
   return s;
 }
 
-// S8 M2M for the internal cells of one level (children in digit order).
+// S8 M2M for the internal cells of one level: one block per parent; the children's
+// shift harmonics (item = (child, m)) and terms (item = (child, coefficient)) are
+// computed in parallel, then each coefficient sums its children in digit order.
 __global__ void m2m_kernel(int64_t lb, const int32_t* __restrict__ child, const int32_t* __restrict__ nchild,
                            const double4* __restrict__ center, int p, int nc, double2* __restrict__ M) {
-  extern __shared__ double2 sh[];  // R[nc], Mc[nc]
+  extern __shared__ double2 sh[];  // R[8][nc], Mc[8][nc], part[8][nc]
   double2* R = sh;
-  double2* Mc = sh + nc;
+  double2* Mc = sh + 8 * nc;
+  double2* part = sh + 16 * nc;
   const int64_t cell = lb + blockIdx.x;
   const int c0 = child[cell];
   if (c0 < 0) return;  // leaf: P2M already wrote M
   const int nch = nchild[cell];
   const double4 cp = center[cell];
-  const int t0 = threadIdx.x, t1 = threadIdx.x + kExpThreads;
-  int j0 = 0, k0 = 0, j1 = 0, k1 = 0;
-  if (t0 < nc) decode_jk(t0, j0, k0);
-  if (t1 < nc) decode_jk(t1, j1, k1);
-  double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
-  for (int ch = c0; ch < c0 + nch; ++ch) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double4 cc = center[ch];
-      regular_harmonics(cc.x - cp.x, cc.y - cp.y, cc.z - cp.z, p, R);
-    }
-    for (int t = threadIdx.x; t < nc; t += blockDim.x) Mc[t] = M[(int64_t)ch * nc + t];
-    __syncthreads();
-    if (t0 < nc) a0 = cadd(a0, m2m_term(R, Mc, j0, k0));
-    if (t1 < nc) a1 = cadd(a1, m2m_term(R, Mc, j1, k1));
+  for (int t = threadIdx.x; t < nch * nc; t += blockDim.x) Mc[t] = M[(int64_t)c0 * nc + t];
+  for (int it = threadIdx.x; it < nch * (p + 1); it += blockDim.x) {
+    const int ch = it / (p + 1), m = it - ch * (p + 1);
+    const double4 cc = center[c0 + ch];
+    regular_column(cc.x - cp.x, cc.y - cp.y, cc.z - cp.z, m, p, R + ch * nc);
   }
-  if (t0 < nc) M[cell * nc + t0] = a0;
-  if (t1 < nc) M[cell * nc + t1] = a1;
+  __syncthreads();
+  for (int it = threadIdx.x; it < nch * nc; it += blockDim.x) {
+    const int ch = it / nc, t = it - ch * nc;
+    int j, k;
+    decode_jk(t, j, k);
+    part[it] = m2m_term(R + ch * nc, Mc + ch * nc, j, k);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+    double2 a = make_double2(0, 0);
+    for (int ch = 0; ch < nch; ++ch) a = cadd(a, part[ch * nc + t]);
+    M[cell * nc + t] = a;
+  }
 }
 
 // M2L term for output (j, k): sum_{n<=p} (-1)^n sum_{|m|<=n} M_n^m I_{j+n}^{k+m}(cB - cA)
@@ -140,24 +150,32 @@ __device__ __forceinline__ double2 l2l_term(const double2* Lp, const double2* R,
   return s;
 }
 
-// S10 L2L for all cells of one level (adds the parent's shifted local expansion).
-__global__ void l2l_kernel(int64_t lb, const int32_t* __restrict__ parent, const double4* __restrict__ center,
-                           int p, int nc, double2* __restrict__ L) {
-  extern __shared__ double2 sh[];  // R[nc], Lp[nc]
+// S10 L2L for the children of one level's internal cells: one block per parent, shift
+// harmonics column-parallel, item = (child, coefficient); each child coefficient is
+// written by exactly one thread.
+__global__ void l2l_kernel(int64_t lb, const int32_t* __restrict__ child, const int32_t* __restrict__ nchild,
+                           const double4* __restrict__ center, int p, int nc, double2* __restrict__ L) {
+  extern __shared__ double2 sh[];  // R[8][nc], Lp[nc]
   double2* R = sh;
-  double2* Lp = sh + nc;
+  double2* Lp = sh + 8 * nc;
   const int64_t cell = lb + blockIdx.x;
-  const int par = parent[cell];
-  if (threadIdx.x == 0) {
-    const double4 cc = center[cell], cp = center[par];
-    regular_harmonics(cc.x - cp.x, cc.y - cp.y, cc.z - cp.z, p, R);
+  const int c0 = child[cell];
+  if (c0 < 0) return;
+  const int nch = nchild[cell];
+  const double4 cp = center[cell];
+  for (int t = threadIdx.x; t < nc; t += blockDim.x) Lp[t] = L[cell * nc + t];
+  for (int it = threadIdx.x; it < nch * (p + 1); it += blockDim.x) {
+    const int ch = it / (p + 1), m = it - ch * (p + 1);
+    const double4 cc = center[c0 + ch];
+    regular_column(cc.x - cp.x, cc.y - cp.y, cc.z - cp.z, m, p, R + ch * nc);
   }
-  for (int t = threadIdx.x; t < nc; t += blockDim.x) Lp[t] = L[(int64_t)par * nc + t];
   __syncthreads();
-  for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+  for (int it = threadIdx.x; it < nch * nc; it += blockDim.x) {
+    const int ch = it / nc, t = it - ch * nc;
     int j, k;
     decode_jk(t, j, k);
-    L[cell * nc + t] = cadd(L[cell * nc + t], l2l_term(Lp, R, p, j, k));
+    double2* dst = L + (int64_t)(c0 + ch) * nc + t;
+    *dst = cadd(*dst, l2l_term(Lp, R + ch * nc, p, j, k));
   }
 }
 
@@ -173,10 +191,16 @@ void upward(fmm_plan_s& P) {
         P.leaves, P.cells.begin, P.cells.end, P.cells.center, P.pos, P.p, nc, P.M);
     FMM_LAUNCHED("p2m_kernel");
   }
+  const size_t sh = sizeof(double2) * 24 * nc;
+  static size_t configured = 0;
+  if (sh > 48 * 1024 && sh > configured) {
+    FMM_CUDA(cudaFuncSetAttribute(m2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+    configured = sh;
+  }
   for (int l = P.max_level - 1; l >= 0; --l) {
     const int64_t lb = P.level_begin[l], le = P.level_begin[l + 1];
-    m2m_kernel<<<(unsigned)(le - lb), kExpThreads, sizeof(double2) * 2 * nc, s>>>(lb, P.cells.child, P.cells.nchild,
-                                                                                  P.cells.center, P.p, nc, P.M);
+    m2m_kernel<<<(unsigned)(le - lb), kM2MThreads, sh, s>>>(lb, P.cells.child, P.cells.nchild, P.cells.center, P.p,
+                                                            nc, P.M);
     FMM_LAUNCHED("m2m_kernel");
   }
 }
@@ -191,10 +215,11 @@ void m2l_pass(fmm_plan_s& P) {
 
 void downward(fmm_plan_s& P) {
   const int nc = P.nc;
-  for (int l = 1; l <= P.max_level; ++l) {
+  const size_t sh = sizeof(double2) * 9 * nc;
+  for (int l = 0; l < P.max_level; ++l) {
     const int64_t lb = P.level_begin[l], le = P.level_begin[l + 1];
-    l2l_kernel<<<(unsigned)(le - lb), kExpThreads, sizeof(double2) * 2 * nc, P.stream>>>(lb, P.cells.parent,
-                                                                                        P.cells.center, P.p, nc, P.L);
+    l2l_kernel<<<(unsigned)(le - lb), kM2MThreads, sh, P.stream>>>(lb, P.cells.child, P.cells.nchild, P.cells.center,
+                                                                   P.p, nc, P.L);
     FMM_LAUNCHED("l2l_kernel");
   }
 }

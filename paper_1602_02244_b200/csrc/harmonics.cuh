@@ -19,6 +19,38 @@ constexpr InvNM make_inv_nm() {
   return t;
 }
 static __constant__ InvNM c_inv_nm = make_inv_nm();
+// -1 / (2m): the diagonal step R_m^m = -(x+iy)/(2m) R_{m-1}^{m-1}
+struct HalfInv {
+  double v[kMaxP + 1];
+};
+constexpr HalfInv make_half_inv() {
+  HalfInv t{};
+  for (int m = 1; m <= kMaxP; ++m) t.v[m] = -0.5 / m;
+  return t;
+}
+static __constant__ HalfInv c_half_inv = make_half_inv();
+
+// Column m (n = m..p) of the regular harmonics R_n^m(x,y,z) into R (m >= 0 storage);
+// columns are independent, so a block computes all of them in parallel.
+__device__ inline void regular_column(double x, double y, double z, int m, int p, double2* R) {
+  const double r2 = x * x + y * y + z * z;
+  double2 d = make_double2(1.0, 0.0);
+  for (int k = 1; k <= m; ++k) {
+    const double s = c_half_inv.v[k];
+    d = cmul(d, make_double2(s * x, s * y));
+  }
+  R[cidx(m, m)] = d;
+  if (m + 1 > p) return;
+  double2 a = d, b = cscale(d, z);
+  R[cidx(m + 1, m)] = b;
+  for (int n = m + 2; n <= p; ++n) {
+    const double inv = c_inv_nm.v[n * (kMaxP + 1) + m];
+    const double2 c = make_double2(((2 * n - 1) * z * b.x - r2 * a.x) * inv, ((2 * n - 1) * z * b.y - r2 * a.y) * inv);
+    R[cidx(n, m)] = c;
+    a = b;
+    b = c;
+  }
+}
 
 // Regular harmonics R_n^m(x,y,z), n <= p, written by ONE thread into R.
 __device__ inline void regular_harmonics(double x, double y, double z, int p, double2* R) {
@@ -92,7 +124,7 @@ __device__ __forceinline__ void l2p_eval(const double2* __restrict__ Lc, int p, 
   double2 g1 = make_double2(0.0, 0.0);
   for (int m = 0; m <= p; ++m) {
     if (m > 0) {
-      const double s = -0.5 / m;
+      const double s = c_half_inv.v[m];
       diag = cmul(diag, make_double2(s * x, s * y));
     }
     const double w = m == 0 ? 1.0 : 2.0;

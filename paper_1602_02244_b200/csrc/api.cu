@@ -125,7 +125,7 @@ void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
   fmm::gather_charges(P, q);
   fmm::upward(P);
   T.mark(1);
-  if (P.m2l_variant == 2)
+  if (P.m2l_variant >= 2)
     fmm::m2l_dmma_pass(P);
   else
     fmm::m2l_pass(P);
@@ -213,12 +213,12 @@ fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncr
     order_leaves_by_position(*P);
     choose_own_range(*P);
     const char* v = getenv("FMM_M2L_VARIANT");
-    if (v && v[0] == '1') P->m2l_variant = 1;
+    if (v && v[0] >= '1' && v[0] <= '3') P->m2l_variant = v[0] - '0';
     const char* nv = getenv("FMM_NEAR_VARIANT");
     if (nv && nv[0] == '1') P->near_variant = 1;
     const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // test hook: export M2L-only local expansions
     P->debug_skip_l2l = dbg && dbg[0] == '1';
-    if (P->m2l_variant == 2) fmm::m2l_dmma_setup(*P);
+    if (P->m2l_variant >= 2) fmm::m2l_dmma_setup(*P);
     P->M.alloc(P->cells.n * P->nc);
     P->L.alloc(P->cells.n * P->nc);
     FMM_CUDA(cudaEventRecord(e3, P->stream));

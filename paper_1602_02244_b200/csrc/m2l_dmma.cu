@@ -34,24 +34,18 @@
 #include <vector>
 
 #include "harmonics.cuh"
+#include "m2l_common.cuh"
 #include "plan.h"
 
 namespace fmm {
+namespace m2l {
+std::vector<int32_t> build_symtab(int p);
+}
+void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a);
 namespace {
+using namespace m2l;
 
 constexpr int kNC = 64;  // max columns per chunk (8 n-tiles of 8)
-
-__host__ __device__ inline int real_count(int p) { return (p + 1) * (p + 1); }
-
-// real index -> (n, m, part)
-__host__ __device__ inline void real_decode(int r, int& n, int& m, int& part) {
-  n = 0;
-  while ((n + 1) * (n + 1) <= r) ++n;
-  const int t = r - n * n;
-  m = (t + 1) >> 1;
-  part = t > 0 ? ((t + 1) & 1) : 0;
-}
-__host__ __device__ inline int real_index(int n, int m, int part) { return m == 0 ? n * n : n * n + 2 * m - 1 + part; }
 
 // ------------------------------------------------------------- symmetry tables (host)
 // A 2x2 signed permutation acting on (re, im).
@@ -89,30 +83,6 @@ M2 dmap(int g, int n, int m, bool local) {
   if (g & 4) D = mul(elementary(2, n, m, local), D);
   if (g & 8) D = mul(elementary(3, n, m, local), D);
   return D;
-}
-
-// packed entry: bits 0..15 source real index, bit 16 = negative sign
-std::vector<int32_t> build_symtab(int p) {
-  const int NR = real_count(p);
-  std::vector<int32_t> t(16 * 2 * NR);
-  for (int g = 0; g < 16; ++g)
-    for (int which = 0; which < 2; ++which) {  // 0: X = (D^M)^{-1} M, 1: L += D^L Y
-      for (int n = 0; n <= p; ++n)
-        for (int m = 0; m <= n; ++m) {
-          M2 D = dmap(g, n, m, which == 1);
-          if (which == 0) D = {D.a, D.c, D.b, D.d};  // inverse of a signed permutation = transpose
-          // out = D * in on (re, im); m == 0 keeps only re (the map is diagonal there)
-          for (int po = 0; po < (m == 0 ? 1 : 2); ++po) {
-            const int c0 = po == 0 ? D.a : D.c, c1 = po == 0 ? D.b : D.d;
-            int src_part = c0 != 0 ? 0 : 1;
-            int sgn = c0 != 0 ? c0 : c1;
-            if (m == 0) src_part = 0, sgn = D.a;
-            const int ro = real_index(n, m, po), rs = real_index(n, m, src_part);
-            t[(g * 2 + which) * NR + ro] = rs | (sgn < 0 ? (1 << 16) : 0);
-          }
-        }
-    }
-  return t;
 }
 
 // ------------------------------------------------------------- setup kernels
@@ -313,29 +283,6 @@ __global__ void hpow_kernel(double S, int p, double* __restrict__ tab) {
 }
 
 // ------------------------------------------------------------- the mat-vec kernel
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
-struct M2LArgs {
-  const double* ops;
-  const int32_t* col_src;
-  const int32_t* col_meta;
-  const int32_t* chunk_begin;
-  const int32_t* chunk_class;
-  const int32_t* chunk_seg;  // [nchunks + 1] first slot segment of each chunk
-  const int32_t* seg_begin;  // [nseg + 1] first column of each segment (global index)
-  const int32_t* tile_chunk;
-  const int32_t* tile_cells;
-  const int32_t* symtab;  // [16][2][NR]
-  const double* hpow;     // [22][p+2]
-  const int32_t* level;
-  const double* Mt;       // [ncells][Kpad] scaled real-form multipoles
-  double2* L;
-  int p, nc, NR, NRpad, Kpad, nks, nmt, T, NC, ystride;
-};
 
 // S9 pre-pass: M~ rows in the real basis, M~[c][r] = {Re,Im} M_n^m(c) h_c^{-n}, zero for r >= NR.
 __global__ void mtilde_kernel(const double2* __restrict__ M, const int32_t* __restrict__ level,
@@ -469,22 +416,6 @@ __device__ __forceinline__ void gather_cols(double* xb, int ncol, const int32_t*
   }
 }
 
-// per-row output transform for all 16 g: bit 2g = take the re/im partner row, bit 2g+1 = negate
-__device__ __forceinline__ uint32_t ltrans_mask(const int32_t* sym, int NR, int r, int& partner_off) {
-  uint32_t mask = 0;
-  partner_off = 0;
-  for (int g = 0; g < 16; ++g) {
-    const int ent = sym[(g * 2 + 1) * NR + r];
-    const int src = ent & 0xffff;
-    if (src != r) {
-      partner_off = src - r;
-      mask |= 1u << (2 * g);
-    }
-    if (ent >> 16) mask |= 2u << (2 * g);
-  }
-  return mask;
-}
-
 // acc[slot][r] += sum over the chunk's columns of (D^L_g Y)[r], segments [s_lo, s_hi) of this thread
 __device__ __forceinline__ void accumulate_rows(double* acc, const double* y, int S, int NR, int r, uint32_t mask,
                                                 int poff, const int32_t* meta, const int32_t* sb,
@@ -524,19 +455,6 @@ __device__ __forceinline__ void writeback(const M2LArgs& a, const double* acc, c
     const double v = acc[e] * a.hpow[a.level[cell] * (a.p + 2) + ((d >> 1) & 0x7f) + 1];
     ((double*)(a.L + (int64_t)cell * a.nc))[2 * (d >> 8) + (d & 1)] = v;
   }
-}
-
-// chunk metadata (columns + slot segments) into buffer slot b
-__device__ __forceinline__ void load_meta_dev(const M2LArgs& a, int ch, int32_t* meta, int32_t* srcs, int32_t* sslot,
-                                              int32_t* sbeg, int t0, int nt) {
-  const int cb = a.chunk_begin[ch], ncol = a.chunk_begin[ch + 1] - cb;
-  const int s0 = a.chunk_seg[ch], ns = a.chunk_seg[ch + 1] - s0;
-  for (int t = t0; t < a.NC; t += nt) {
-    meta[t] = t < ncol ? a.col_meta[cb + t] : 0;
-    srcs[t] = t < ncol ? a.col_src[cb + t] : 0;
-    if (t < ns) sslot[t] = a.col_meta[a.seg_begin[s0 + t]] & 0xff;
-  }
-  for (int t = t0; t <= ns; t += nt) sbeg[t] = a.seg_begin[s0 + t] - cb;
 }
 
 // shared-memory carve-up common to both kernels
@@ -629,11 +547,6 @@ __global__ void __launch_bounds__(640, 1) m2l_dmma_kernel(const M2LArgs a) {
 //   Yfull(i):  MMA bar.arrive after staging Y(i);      helpers bar.sync before adding Y(i)
 // Y(i) is staged over X[i % 2] (consumed by GEMM(i)); helpers overwrite X[i % 2] with
 // X(i+2) only after adding Y(i), so two X buffers suffice.
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void named_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
 __global__ void __launch_bounds__(512, 1) m2l_ws_kernel(const M2LArgs a, int nmma, int nhelp, int dbg) {
   extern __shared__ double sm[];
   const Smem m = carve(sm, a);
@@ -833,6 +746,33 @@ __global__ void seg_emit_kernel(const int32_t* __restrict__ sflag, const int64_t
 
 }  // namespace
 
+namespace m2l {
+// packed entry: bits 0..15 source real index, bit 16 = negative sign
+std::vector<int32_t> build_symtab(int p) {
+  const int NR = real_count(p);
+  std::vector<int32_t> t(16 * 2 * NR);
+  for (int g = 0; g < 16; ++g)
+    for (int which = 0; which < 2; ++which) {  // 0: X = (D^M)^{-1} M, 1: L += D^L Y
+      for (int n = 0; n <= p; ++n)
+        for (int m = 0; m <= n; ++m) {
+          M2 D = dmap(g, n, m, which == 1);
+          if (which == 0) D = {D.a, D.c, D.b, D.d};  // inverse of a signed permutation = transpose
+          // out = D * in on (re, im); m == 0 keeps only re (the map is diagonal there)
+          for (int po = 0; po < (m == 0 ? 1 : 2); ++po) {
+            const int c0 = po == 0 ? D.a : D.c, c1 = po == 0 ? D.b : D.d;
+            int src_part = c0 != 0 ? 0 : 1;
+            int sgn = c0 != 0 ? c0 : c1;
+            if (m == 0) src_part = 0, sgn = D.a;
+            const int ro = real_index(n, m, po), rs = real_index(n, m, src_part);
+            t[(g * 2 + which) * NR + ro] = rs | (sgn < 0 ? (1 << 16) : 0);
+          }
+        }
+    }
+  return t;
+}
+
+}  // namespace m2l
+
 size_t m2l_smem_bytes(const M2LDmma& D) {
   return ((size_t)D.T * D.NR + 2 * (size_t)D.ystride * D.NC) * sizeof(double) +
          (8 * D.NC + 2 + 35 * D.NR) * sizeof(int32_t);
@@ -854,6 +794,11 @@ void m2l_dmma_setup(fmm_plan_s& P) {
   if (2 * (size_t)D.ystride * D.NC * sizeof(double) > 140 * 1024) D.NC = kNC / 2;  // large p: 32-column chunks
   D.T = 64;
   while (D.T > 8 && m2l_smem_bytes(D) > 220 * 1024) D.T /= 2;
+  if (P.m2l_variant == 3 && !(m2l_rot_supported(p) && rot_chunk_width(p) == D.NC)) P.m2l_variant = 2;
+  if (P.m2l_variant == 3) {
+    D.T = 64;
+    while (D.T > 8 && rot_smem_bytes(p, D.T, 24) > 225 * 1024) D.T /= 2;
+  }
   // warp-specialised kernel: nmt/2 MMA warps + ceil(NR/32) helper warps, <= 512 threads
   D.nhelp = std::min(2 * ((D.NR + 31) / 32), 16 - D.nmt / 2);
   D.use_ws = D.nhelp >= 1 && D.NR > 32 && D.Kpad <= 256 && getenv("FMM_M2L_NO_WS") == nullptr;
@@ -901,18 +846,20 @@ void m2l_dmma_setup(fmm_plan_s& P) {
   diff_flag_kernel<<<cdiv(n, 256), 256, 0, s>>>(keys, n, pflag);
   FMM_LAUNCHED("diff_flag_kernel");
   D.nclass = scan_counts_total(pflag, poff, n, s);
-  DevBuf<uint64_t> ckeys;
-  ckeys.alloc(D.nclass);
+  D.class_keys.alloc(D.nclass);
+  DevBuf<uint64_t>& ckeys = D.class_keys;
   class_assign_kernel<<<cdiv(n, 256), 256, 0, s>>>(keys, idx, pflag, poff, n, pcls, ckeys);
   FMM_LAUNCHED("class_assign_kernel");
   if (D.nclass >= (1 << 24)) throw Error(FMM_ERR_USAGE, "m2l: too many operator classes");
   if (D.ntiles >= (1 << 28)) throw Error(FMM_ERR_USAGE, "m2l: too many tiles");
 
   // ---- operators (fragment order) and per-level scale table
-  const int64_t opsz = (int64_t)D.nmt * D.nks * 32;
-  D.ops.alloc(D.nclass * opsz);
-  build_ops_kernel<<<(unsigned)D.nclass, 256, sizeof(double2) * ncoef(2 * p), s>>>(ckeys, p, D.nmt, D.nks, D.ops);
-  FMM_LAUNCHED("build_ops_kernel");
+  if (P.m2l_variant == 2) {
+    const int64_t opsz = (int64_t)D.nmt * D.nks * 32;
+    D.ops.alloc(D.nclass * opsz);
+    build_ops_kernel<<<(unsigned)D.nclass, 256, sizeof(double2) * ncoef(2 * p), s>>>(ckeys, p, D.nmt, D.nks, D.ops);
+    FMM_LAUNCHED("build_ops_kernel");
+  }
   D.hpow.alloc((kMaxLevel + 1) * (p + 2));
   hpow_kernel<<<1, 32, 0, s>>>(P.S, p, D.hpow);
   FMM_LAUNCHED("hpow_kernel");
@@ -980,6 +927,7 @@ void m2l_dmma_setup(fmm_plan_s& P) {
   tile_chunk_kernel<<<cdiv(D.nchunks + 1, 256), 256, 0, s>>>(ctile, D.nchunks, D.ntiles, D.tile_chunk);
   FMM_LAUNCHED("tile_chunk_kernel");
   FMM_CUDA(cudaStreamSynchronize(s));
+  if (P.m2l_variant == 3) m2l_rot_setup(P);
 }
 
 void m2l_dmma_pass(fmm_plan_s& P) {
@@ -1015,6 +963,10 @@ void m2l_dmma_pass(fmm_plan_s& P) {
   a.T = D.T;
   a.NC = D.NC;
   a.ystride = D.ystride;
+  if (P.m2l_variant == 3) {
+    m2l_rot_launch(P, a);
+    return;
+  }
   const size_t sh = m2l_smem_bytes(D);
   const int threads = 32 * (D.nmt / 2);
   static size_t configured[2] = {0, 0};  // dynamic-smem opt-in per kernel

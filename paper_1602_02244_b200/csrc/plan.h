@@ -85,10 +85,17 @@ struct M2LDmma {
   DevBuf<int32_t> tile_cells;  // [ntiles * T], -1 padding
   DevBuf<int32_t> symtab;      // [16][2][NR]
   DevBuf<double> hpow;         // [22][p + 2]
+  DevBuf<uint64_t> class_keys; // [nclass] canonical (level difference, offset) keys
+  // M2L v3 (m2l_rot.cu): rotation-factored class operators
+  DevBuf<double> rot_ops;      // [nclass][rot_ops_size(p)] A fragments of the D, Z~, Dt stages
+  DevBuf<double2> rot_az;      // [nclass][p + 1] (cos m alpha, sin m alpha)
+  DevBuf<int32_t> rot_sched;   // [3][8][rot_smax] MMA-warp item lists
+  int rot_smax = 0, rot_T = 0;
   int64_t bytes() const {
     return ops.bytes() + col_src.bytes() + col_meta.bytes() + chunk_begin.bytes() + chunk_class.bytes() +
            tile_chunk.bytes() + tile_cells.bytes() + symtab.bytes() + hpow.bytes() + chunk_seg.bytes() +
-           seg_begin.bytes() + Mt.bytes();
+           seg_begin.bytes() + Mt.bytes() + class_keys.bytes() + rot_ops.bytes() + rot_az.bytes() +
+           rot_sched.bytes();
   }
 };
 
@@ -127,7 +134,8 @@ struct fmm_plan_s {
   fmm::PairList p2p, m2l;
   int64_t n_p2p_interactions = 0;
   fmm::M2LDmma m2l_dmma;
-  int m2l_variant = 2;  // 1 = matrix-free O(p^4) per pair (v1), 2 = DMMA operator classes (v2)
+  int m2l_variant = 3;  // 1 = matrix-free O(p^4) per pair (v1), 2 = dense DMMA operator classes (v2),
+                        // 3 = rotation-factored DMMA operator classes (v3, p = 5..14; else v2)
   int near_variant = 2; // 1 = block per leaf, thread per target (v1), 2 = warp per leaf (v2)
 
   // this rank's targets (Morton range of sorted positions) and its leaves
@@ -157,6 +165,10 @@ void upward(fmm_plan_s& P);
 void m2l_pass(fmm_plan_s& P);
 void m2l_dmma_setup(fmm_plan_s& P);
 void m2l_dmma_pass(fmm_plan_s& P);
+bool m2l_rot_supported(int p);
+void m2l_rot_setup(fmm_plan_s& P);
+size_t rot_smem_bytes(int p, int T, int smax);
+int rot_chunk_width(int p);
 void downward(fmm_plan_s& P);
 void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
 void near_pass_warp(fmm_plan_s& P, double* phi, double* grad);

@@ -42,6 +42,7 @@ namespace m2l {
 std::vector<int32_t> build_symtab(int p);
 }
 void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a);
+void m2l_rot_mtilde(fmm_plan_s& P);
 namespace {
 using namespace m2l;
 
@@ -935,9 +936,13 @@ void m2l_dmma_pass(fmm_plan_s& P) {
   FMM_CUDA(cudaMemsetAsync(P.L.ptr, 0, sizeof(double2) * P.L.count, P.stream));
   if (D.ntiles == 0) return;
   const int64_t ne = P.cells.n * D.Kpad;
-  mtilde_kernel<<<cdiv(ne, 256), 256, 0, P.stream>>>(P.M, P.cells.level, D.hpow, P.cells.n, P.p, P.nc, D.NR, D.Kpad,
-                                                     D.Mt);
-  FMM_LAUNCHED("mtilde_kernel");
+  if (P.m2l_variant == 3) {
+    m2l_rot_mtilde(P);
+  } else {
+    mtilde_kernel<<<cdiv(ne, 256), 256, 0, P.stream>>>(P.M, P.cells.level, D.hpow, P.cells.n, P.p, P.nc, D.NR, D.Kpad,
+                                                       D.Mt);
+    FMM_LAUNCHED("mtilde_kernel");
+  }
   M2LArgs a;
   a.ops = D.ops;
   a.col_src = D.col_src;

@@ -49,35 +49,55 @@
 namespace fmm {
 namespace m2l {
 
-// --------------------------------------------------------------------- operator layout
-__host__ __device__ inline int frag_count(int R, int K) { return ((R + 7) / 8) * ((K + 3) / 4) * 32; }
-// rows (= K) of block blk in stage st: stages 0/2 (rotations) degree n = blk -> n + 1;
-// stage 1 (z translation) order m = blk -> p + 1 - m
+// --------------------------------------------------------------------- class data layout
+// One class's data ("blob", doubles): az[p+1] (cos m a, sin m a) | per degree n: D_re (n+1)^2
+// row-major, D_im (n+1)^2 (row/column 0 zero) | per order m: Z~_m (p+1-m)^2 row-major;
+// padded to an even count (16-byte bulk copies). Stage st of block blk reads its A operand
+// from it: st 0 D, st 1 Z~, st 2 D transposed (Re: E^-1 D^T E).
 __host__ __device__ inline int rot_block_rows(int p, int st, int blk) { return st == 1 ? p + 1 - blk : blk + 1; }
 __host__ __device__ inline int rot_block_parts(int st, int blk) { return st == 1 ? 1 : (blk > 0 ? 2 : 1); }
-// offset (doubles) of (st, blk, part) inside one class's operator set; total at (3, 0, 0)
-__host__ __device__ inline int rot_block_offset(int p, int st, int blk, int part) {
-  int off = 0;
-  for (int s = 0; s < 3; ++s)
-    for (int b = 0; b <= p; ++b)
-      for (int pt = 0; pt < rot_block_parts(s, b); ++pt) {
-        if (s == st && b == blk && pt == part) return off;
-        const int R = rot_block_rows(p, s, b);
-        off += frag_count(R, R);
-      }
+__host__ __device__ constexpr int rot_d_offset(int p, int n, int part) {
+  int off = 2 * (p + 1);
+  for (int k = 0; k < n; ++k) off += 2 * (k + 1) * (k + 1);
+  return off + part * (n + 1) * (n + 1);
+}
+__host__ __device__ constexpr int rot_z_offset(int p, int m) {
+  int off = rot_d_offset(p, p + 1, 0);
+  for (int k = 0; k < m; ++k) off += (p + 1 - k) * (p + 1 - k);
   return off;
 }
-__host__ __device__ inline int rot_ops_size(int p) { return rot_block_offset(p, 3, 0, 0); }
+__host__ __device__ constexpr int rot_blob_size(int p) { return (rot_z_offset(p, p + 1) + 1) & ~1; }
+__host__ __device__ inline int rot_block_offset(int p, int st, int blk, int part) {
+  return st == 1 ? rot_z_offset(p, blk) : rot_d_offset(p, blk, part);
+}
 
-// position (real index) of row/column index r of block (st, blk, part); -1 = none (zero)
+// "RI" layout of one expansion in the M2L v3 kernel (and of M~ rows): a Re plane
+// (n, m >= 0) at n(n+1)/2 + m followed by an Im plane (n, m >= 1) at nc + n(n-1)/2 + m - 1;
+// (p+1)^2 doubles, and both rotation stages read/write runs contiguous in m.
+__host__ __device__ inline int ri_pos(int p, int n, int m, int part) {
+  return part == 0 ? n * (n + 1) / 2 + m : (p + 1) * (p + 2) / 2 + n * (n - 1) / 2 + m - 1;
+}
+__host__ __device__ inline void ri_decode(int p, int q, int& n, int& m, int& part) {
+  const int nc = (p + 1) * (p + 2) / 2;
+  part = q >= nc;
+  if (part) q -= nc;
+  n = part;
+  while ((part ? (n + 1) * n / 2 : (n + 1) * (n + 2) / 2) <= q) ++n;
+  m = part ? q - n * (n - 1) / 2 + 1 : q - n * (n + 1) / 2;
+}
+// position of row/column index r of block (st, blk, part); -1 = none (zero)
 __host__ __device__ inline int rot_pos(int p, int st, int blk, int part, int r) {
   if (st == 1) {  // order m = blk, degree n = m + r
     if (r > p - blk) return -1;
-    return real_index(blk + r, blk, part);
+    return ri_pos(p, blk + r, blk, part);
   }
   if (r > blk || (part == 1 && r == 0)) return -1;  // degree n = blk, order m = r
-  return real_index(blk, r, part);
+  return ri_pos(p, blk, r, part);
 }
+// column base in a chunk buffer: stride S (= 4 mod 16 doubles) plus a +-4 swizzle on columns
+// 4..7 of every 8, so B-fragment loads (8 columns x 4 rows) and C-fragment stores (8 rows x
+// columns 2k+e) both hit 16 distinct 8-byte banks per half-warp on contiguous positions
+__host__ __device__ inline int col_base(int c, int S) { return c * S + ((c & 4) ? ((c & 1) ? -4 : 4) : 0); }
 
 }  // namespace m2l
 
@@ -106,7 +126,7 @@ constexpr int kMaxEntPerThread = 13;  // ceil(sum_n (n+1)^2 + n^2 at p = 16 / 25
 // stages in DMMA A-fragment order (A[8 mt + lane/4][4 ks + lane%4]).
 __global__ void __launch_bounds__(kRotBuildThreads) build_rot_ops_kernel(
     const uint64_t* __restrict__ class_keys, int p, const double* __restrict__ glx, const double* __restrict__ glw,
-    const double2* __restrict__ Rs, double* __restrict__ ops, double2* __restrict__ az) {
+    const double2* __restrict__ Rs, double* __restrict__ blobs) {
   extern __shared__ double2 sh[];  // Rq[kQuadBatch][nc], then D[nent] (doubles)
   const int nc = ncoef(p), nphi = 2 * p + 1, np = (p + 1) * nphi;
   double2* Rq = sh;
@@ -120,10 +140,12 @@ __global__ void __launch_bounds__(kRotBuildThreads) build_rot_ops_kernel(
   const double alpha = atan2(y0, x0), beta = atan2(rxy, z0);
   const double cb = cos(beta), sb = sin(beta);
   const double fA = dl < 0 ? ldexp(1.0, -dl) : 1.0, fB = dl > 0 ? ldexp(1.0, dl) : 1.0;
+  double* out = blobs + (int64_t)cls * rot_blob_size(p);
   if (tid <= p) {
     double s, c;
     sincos(tid * alpha, &s, &c);
-    az[(int64_t)cls * (p + 1) + tid] = make_double2(c, s);
+    out[2 * tid] = c;
+    out[2 * tid + 1] = s;
   }
   // entries e -> (n, part, a, b): per degree n the Re block (a, b in 0..n) then the Im
   // block (a, b in 1..n)
@@ -192,54 +214,46 @@ __global__ void __launch_bounds__(kRotBuildThreads) build_rot_ops_kernel(
     Dtab[e] = (2.0 * n + 1.0) / nphi * c2 * acc[q];
   }
   __syncthreads();
-  // fragments
-  double* out = ops + (int64_t)cls * rot_ops_size(p);
-  for (int st = 0; st < 3; ++st)
-    for (int blk = 0; blk <= p; ++blk)
-      for (int part = 0; part < rot_block_parts(st, blk); ++part) {
-        const int R = rot_block_rows(p, st, blk), KS = (R + 3) / 4, MT = (R + 7) / 8;
-        double* o = out + rot_block_offset(p, st, blk, part);
-        int base = 0;  // start of degree blk in Dtab
-        for (int n = 0; n < blk; ++n) base += (n + 1) * (n + 1) + n * n;
-        for (int e = tid; e < MT * KS * 32; e += blockDim.x) {
-          const int lane = e & 31, fr = e >> 5, ks = fr % KS, mt = fr / KS;
-          const int r = 8 * mt + (lane >> 2), k = 4 * ks + (lane & 3);
-          double v = 0.0;
-          if (r < R && k < R) {
-            if (st == 1) {  // Z~_m[i][k]: j = m + i, n = m + k
-              const int m = blk, j = m + r, n = m + k;
-              double g = 1.0 / rho;  // (j+n)! / rho^{j+n+1}
-              for (int l = 1; l <= j + n; ++l) g *= l / rho;
-              for (int t = 0; t <= j; ++t) g *= fA;
-              for (int t = 0; t < n; ++t) g *= fB;
-              v = ((n + m) & 1) ? -g : g;
-            } else {
-              const int n = blk;
-              int rr = st == 0 ? r : k, kk = st == 0 ? k : r;  // stage 2: transpose
-              if (part == 0) {
-                v = Dtab[base + rr * (n + 1) + kk];
-                if (st == 2) v *= (rr == 0 ? 1.0 : 2.0) / (kk == 0 ? 1.0 : 2.0);  // (E^-1 D^T E)[r][k] = D[k][r] E_k / E_r
-              } else if (rr > 0 && kk > 0) {
-                v = Dtab[base + (n + 1) * (n + 1) + (rr - 1) * n + (kk - 1)];
-              }
-            }
-          }
-          o[e] = v;
-        }
-      }
+  // D blocks (Re, Im with zero row/column 0) and Z~ blocks, row-major
+  for (int n = 0; n <= p; ++n) {
+    int base = 0;  // start of degree n in Dtab
+    for (int k = 0; k < n; ++k) base += (k + 1) * (k + 1) + k * k;
+    const int R = n + 1;
+    for (int e = tid; e < 2 * R * R; e += blockDim.x) {
+      const int part = e / (R * R), rr = (e / R) % R, kk = e % R;
+      double v = 0.0;
+      if (part == 0)
+        v = Dtab[base + rr * R + kk];
+      else if (rr > 0 && kk > 0)
+        v = Dtab[base + R * R + (rr - 1) * n + (kk - 1)];
+      out[rot_d_offset(p, n, part) + rr * R + kk] = v;
+    }
+  }
+  for (int m = 0; m <= p; ++m) {
+    const int R = p + 1 - m;
+    for (int e = tid; e < R * R; e += blockDim.x) {
+      const int i = e / R, k = e % R, j = m + i, n = m + k;
+      double g = 1.0 / rho;  // (j+n)! / rho^{j+n+1}
+      for (int l = 1; l <= j + n; ++l) g *= l / rho;
+      for (int t = 0; t <= j; ++t) g *= fA;
+      for (int t = 0; t < n; ++t) g *= fB;
+      out[rot_z_offset(p, m) + e] = ((n + m) & 1) ? -g : g;
+    }
+  }
+  if (tid == 0 && (rot_z_offset(p, p + 1) & 1)) out[rot_z_offset(p, p + 1)] = 0.0;
 }
 
 // ------------------------------------------------------------------- the mat-vec kernel
 struct RotArgs {
   M2LArgs a;
-  const double* rops;    // [nclass][rot_ops_size(p)]
-  const double2* raz;    // [nclass][p + 1]
+  const double* blobs;   // [nclass][rot_blob_size(p)] class data (azimuths, D and Z~ blocks)
+  const uint32_t* masks; // [2][NR] symmetry masks: 0 = multipole side (inverse map), 1 = local side
   const int32_t* sched;  // [3][nmma][smax] items (-1 = end)
   int smax, S;
 };
 
 constexpr int rot_xstride(int kpad) {
-  int s = kpad + 1;
+  int s = kpad + 8;  // room for the +-4 column swizzle
   while (s % 16 != 4) ++s;
   return s;
 }
@@ -247,8 +261,7 @@ template <int P>
 struct RGeo {
   static constexpr int NR = (P + 1) * (P + 1);
   static constexpr int KPAD = (NR + 3) & ~3;
-  static constexpr int S = rot_xstride(KPAD);  // column stride; position KPAD is the zero slot
-  static constexpr int ZERO = KPAD;
+  static constexpr int S = rot_xstride(KPAD);  // column stride (see col_base)
   static constexpr int NC = 2 * S * 64 * 8 > 140 * 1024 ? 32 : 64;  // as v2's chunk width rule
   static constexpr int NMMA = 8;
   static constexpr int MTMAX = (P + 1 + 7) / 8;
@@ -257,10 +270,10 @@ struct RGeo {
 };
 
 struct RotSmem {
-  double *acc, *x0, *x1;
-  double2* azs;  // [2][P+1]
-  int32_t *meta, *srcs, *sslot, *sbeg, *sym, *dec, *lmask, *lpoff, *pairtab, *sched, *ccls, *blkoff;
-  uint64_t* bar;  // [2]
+  double *acc, *x0, *x1, *ob;  // ob: [2][blob] class data of the chunk in each buffer
+  uint64_t* bar;               // [2]
+  int32_t *meta, *srcs, *sslot, *sbeg, *dec, *pairtab, *sched, *blkoff;
+  uint32_t *mmask, *lmask;     // [NR] symmetry masks (bit 2g: take re/im partner, 2g+1: negate)
 };
 template <int P>
 __device__ __forceinline__ RotSmem rot_carve(double* sm, const RotArgs& r) {
@@ -269,29 +282,27 @@ __device__ __forceinline__ RotSmem rot_carve(double* sm, const RotArgs& r) {
   m.acc = sm;
   m.x0 = m.acc + (size_t)r.a.T * G::NR;
   m.x1 = m.x0 + G::NC * G::S;
-  m.azs = (double2*)(m.x1 + G::NC * G::S);
-  uint64_t* b = (uint64_t*)(m.azs + 2 * (P + 1));
+  m.ob = m.x1 + G::NC * G::S;
+  uint64_t* b = (uint64_t*)(m.ob + 2 * rot_blob_size(P));
   m.bar = b;
   m.meta = (int32_t*)(b + 2);
   m.srcs = m.meta + 2 * G::NC;
   m.sslot = m.srcs + 2 * G::NC;
   m.sbeg = m.sslot + 2 * G::NC;
-  m.sym = m.sbeg + 2 * (G::NC + 1);
-  m.dec = m.sym + 32 * G::NR;
-  m.lmask = m.dec + G::NR;
-  m.lpoff = m.lmask + G::NR;
-  m.pairtab = m.lpoff + G::NR;
-  m.ccls = m.pairtab + G::NCOEF;
-  m.sched = m.ccls + 2;
-  m.blkoff = m.sched + 3 * G::NMMA * r.smax;  // [3][P+1][2]
+  m.dec = m.sbeg + 2 * (G::NC + 1);
+  m.mmask = (uint32_t*)(m.dec + G::NR);
+  m.lmask = m.mmask + G::NR;
+  m.pairtab = (int32_t*)(m.lmask + G::NR);
+  m.blkoff = m.pairtab + G::NCOEF;      // [3][P+1][2]
+  m.sched = m.blkoff + 6 * (P + 1);
   return m;
 }
 }  // namespace
 size_t rot_smem_bytes(int p, int T, int smax) {
   const int NR = (p + 1) * (p + 1), KPAD = (NR + 3) & ~3, S = rot_xstride(KPAD), nc = ncoef(p);
   const int NC = 2 * S * 64 * 8 > 140 * 1024 ? 32 : 64;
-  return sizeof(double) * ((size_t)T * NR + 2 * NC * (size_t)S) + sizeof(double2) * 2 * (p + 1) +
-         sizeof(uint64_t) * 2 + sizeof(int32_t) * (8 * NC + 2 + 35 * NR + nc + 2 + 3 * 8 * smax + 6 * (p + 1));
+  return sizeof(double) * ((size_t)T * NR + 2 * NC * (size_t)S + 2 * (size_t)rot_blob_size(p)) +
+         sizeof(uint64_t) * 2 + sizeof(int32_t) * (8 * NC + 2 + 3 * NR + nc + 6 * (p + 1) + 3 * 8 * smax);
 }
 int rot_chunk_width(int p) {
   const int NR = (p + 1) * (p + 1), KPAD = (NR + 3) & ~3, S = rot_xstride(KPAD);
@@ -328,72 +339,77 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// One MMA item: block (st, blk), part(s), n-tiles cg, cg + 2, ... of the chunk; in place.
+// One MMA item: block (st, blk), part, all n-tiles of the chunk, in place: the B operand
+// is streamed per k-step, the results stay in registers until every k-step has been read;
+// A operand from the chunk's class data in shared memory.
 template <int P>
-__device__ __forceinline__ void rot_item(const double* __restrict__ ops, const int32_t* blkoff, int st, int blk,
-                                         int part, int cg, int ntiles, double* xc, int lane) {
+__device__ __forceinline__ void rot_item(const double* ob, const int32_t* blkoff, int st, int blk, int pt,
+                                         int ntiles, double* xc, int lane) {
   using G = RGeo<P>;
+  constexpr int NT = G::NC / 8;
   const int R = rot_block_rows(P, st, blk), MT = (R + 7) / 8, KS = (R + 3) / 4;
-  const int np = st == 1 ? (blk > 0 ? 2 : 1) : 1;  // stage 1: Re and Im with the same operator
-  const double* A = ops + blkoff[(st * (P + 1) + blk) * 2 + (st == 1 ? 0 : part)] + lane;
+  const double* A = ob + blkoff[(st * (P + 1) + blk) * 2 + (st == 1 ? 0 : pt)];
+  const int colb = lane >> 2, kl = lane & 3;
   double a[G::MTMAX][G::KSMAX];
 #pragma unroll
   for (int mt = 0; mt < G::MTMAX; ++mt)
 #pragma unroll
-    for (int ks = 0; ks < G::KSMAX; ++ks) a[mt][ks] = (mt < MT && ks < KS) ? __ldg(A + (mt * KS + ks) * 32) : 0.0;
-  const int colb = lane >> 2, kl = lane & 3;
-  for (int pp = 0; pp < np; ++pp) {
-    const int pt = st == 1 ? pp : part;
-    double b[G::KSMAX][4];
-#pragma unroll
     for (int ks = 0; ks < G::KSMAX; ++ks) {
-      int pos = ks < KS ? rot_pos(P, st, blk, pt, 4 * ks + kl) : -1;
-      if (pos < 0) pos = G::ZERO;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int nt = cg + 2 * t;
-        b[ks][t] = (nt < ntiles && ks < KS) ? xc[(8 * nt + colb) * G::S + pos] : 0.0;
-      }
-    }
-    double c[G::MTMAX][4][2];
-#pragma unroll
-    for (int mt = 0; mt < G::MTMAX; ++mt)
-#pragma unroll
-      for (int t = 0; t < 4; ++t) c[mt][t][0] = c[mt][t][1] = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < G::KSMAX; ++ks)
-      if (ks < KS)
-#pragma unroll
-        for (int mt = 0; mt < G::MTMAX; ++mt)
-          if (mt < MT)
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (cg + 2 * t < ntiles) dmma884(c[mt][t][0], c[mt][t][1], a[mt][ks], b[ks][t]);
-    __syncwarp();  // every lane's B loads precede the in-place stores
-    const double sgn = (st == 1 && pt == 1) ? -1.0 : 1.0;
-#pragma unroll
-    for (int mt = 0; mt < G::MTMAX; ++mt) {
-      const int r = 8 * mt + (lane >> 2);
-      const int pos = (mt < MT && r < R) ? rot_pos(P, st, blk, pt, r) : -1;
-      if (pos < 0) continue;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int nt = cg + 2 * t;
-        if (nt < ntiles) {
-          const int col = 8 * nt + 2 * kl;
-          xc[col * G::S + pos] = sgn * c[mt][t][0];
-          xc[(col + 1) * G::S + pos] = sgn * c[mt][t][1];
+      const int rr = 8 * mt + colb, kk = 4 * ks + kl;
+      double v = 0.0;
+      if (mt < MT && ks < KS && rr < R && kk < R) {
+        if (st == 2) {  // transposed; Re: E^-1 D^T E
+          v = A[kk * R + rr];
+          if (pt == 0) v *= (kk == 0 ? 1.0 : 2.0) * (rr == 0 ? 1.0 : 0.5);
+        } else {
+          v = A[rr * R + kk];
         }
       }
+      a[mt][ks] = v;
     }
-    __syncwarp();
+  double c[G::MTMAX][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < G::MTMAX; ++mt)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) c[mt][t][0] = c[mt][t][1] = 0.0;
+  const double* xb = xc + col_base(colb, G::S);
+#pragma unroll
+  for (int ks = 0; ks < G::KSMAX; ++ks) {
+    if (ks < KS) {
+      const int pos = rot_pos(P, st, blk, pt, 4 * ks + kl);
+      double b[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) b[t] = (t < ntiles && pos >= 0) ? xb[8 * t * G::S + pos] : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < G::MTMAX; ++mt)
+        if (mt < MT)
+#pragma unroll
+          for (int t = 0; t < NT; ++t)
+            if (t < ntiles) dmma884(c[mt][t][0], c[mt][t][1], a[mt][ks], b[t]);
+    }
+  }
+  __syncwarp();  // every lane's B loads precede the in-place stores
+  const double sgn = (st == 1 && pt == 1) ? -1.0 : 1.0;
+#pragma unroll
+  for (int mt = 0; mt < G::MTMAX; ++mt) {
+    const int r = 8 * mt + colb;
+    const int pos = (mt < MT && r < R) ? rot_pos(P, st, blk, pt, r) : -1;
+    if (pos < 0) continue;
+    double* y0 = xc + col_base(2 * kl, G::S) + pos;
+    double* y1 = xc + col_base(2 * kl + 1, G::S) + pos;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+      if (t < ntiles) {
+        y0[8 * t * G::S] = sgn * c[mt][t][0];
+        y1[8 * t * G::S] = sgn * c[mt][t][1];
+      }
   }
 }
 
 template <int P>
-__global__ void __launch_bounds__(512, 1) m2l_rot_kernel(const RotArgs r, int nhelp) {
+__global__ void __launch_bounds__(512, 1) m2l_rot_kernel(const RotArgs r, int nhelp, int dbg) {
   using G = RGeo<P>;
-  constexpr int NR = G::NR, NC = G::NC, S = G::S, NCOEF = G::NCOEF;
+  constexpr int NR = G::NR, NC = G::NC, S = G::S, NCOEF = G::NCOEF, BLOB = rot_blob_size(P);
   extern __shared__ double sm[];
   const RotSmem m = rot_carve<P>(sm, r);
   const M2LArgs& a = r.a;
@@ -403,112 +419,106 @@ __global__ void __launch_bounds__(512, 1) m2l_rot_kernel(const RotArgs r, int nh
   const int nhelp_t = 32 * nhelp, nall = nmma_t + nhelp_t;
   // ---- shared tables
   for (int e = tid; e < a.T * NR; e += nthr) m.acc[e] = 0.0;
-  for (int e = tid; e < 32 * NR; e += nthr) m.sym[e] = a.symtab[e];
   for (int q = tid; q < NCOEF; q += nthr) {
     int n = 0;
     while (cidx(n + 1, 0) <= q) ++n;
-    m.pairtab[q] = (n * n) | ((q - cidx(n, 0)) << 16);
+    m.pairtab[q] = n | ((q - cidx(n, 0)) << 16);
   }
   for (int e = tid; e < 3 * G::NMMA * r.smax; e += nthr) m.sched[e] = r.sched[e];
   for (int e = tid; e < 6 * (P + 1); e += nthr) {
     const int st = e / (2 * (P + 1)), blk = (e / 2) % (P + 1), pt = e & 1;
     m.blkoff[e] = pt < rot_block_parts(st, blk) ? rot_block_offset(P, st, blk, pt) : 0;
   }
-  for (int e = tid; e < 2 * NC; e += nthr) {  // zero slots and padding rows of both buffers
-    double* xb = (e < NC ? m.x0 : m.x1) + (e % NC) * S;
-    for (int k = G::KPAD; k < S; ++k) xb[k] = 0.0;
-  }
   for (int q = tid; q < NR; q += nthr) {
     int n, mm, part;
-    real_decode(q, n, mm, part);
+    ri_decode(P, q, n, mm, part);
     m.dec[q] = (cidx(n, mm) << 8) | (n << 1) | part;
+    m.mmask[q] = r.masks[q];
+    m.lmask[q] = r.masks[NR + q];
   }
   if (tid == 0) {
     mbar_init(m.bar, 1);
     mbar_init(m.bar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  for (int q = tid; q < NR; q += nthr) {
-    int poff = 0;
-    m.lmask[q] = (int32_t)ltrans_mask(m.sym, NR, q, poff);
-    m.lpoff[q] = poff;
-  }
   const int c_first = a.tile_chunk[tile], c_last = a.tile_chunk[tile + 1];
   __syncthreads();
   if (warp >= G::NMMA) {
     // ================= helper warps
     const int h = tid - nmma_t;
-    // stage chunk ch into buffer b: metadata, class azimuths, TMA bulk copies, symmetry + Az_M
+    // stage chunk ch into buffer b: metadata; TMA bulk copies of the class data and of the
+    // source multipoles; then the column's symmetry map and Az_M in place
     auto prep = [&](int ch, int b, unsigned parity) {
       double* xb = b ? m.x1 : m.x0;
+      double* ob = m.ob + b * BLOB;
       load_meta_dev(a, ch, m.meta + b * NC, m.srcs + b * NC, m.sslot + b * NC, m.sbeg + b * (NC + 1), h, nhelp_t);
       const int cls = a.chunk_class[ch];
-      if (h <= P) m.azs[b * (P + 1) + h] = r.raz[(int64_t)cls * (P + 1) + h];
       const int ncol = a.chunk_begin[ch + 1] - a.chunk_begin[ch];
       named_sync(6, nhelp_t);  // metadata visible to all helpers
-      if (h < 32) {
-        fence_proxy_async();  // earlier generic accesses of xb before the async-proxy writes
-        if (h == 0) mbar_arrive_tx(m.bar + b, (unsigned)(ncol * G::KPAD * sizeof(double)));
+      if (h < 32 && !(dbg & 8)) {
+        fence_proxy_async();  // earlier generic accesses of xb / ob before the async-proxy writes
+        if (h == 0) {
+          mbar_arrive_tx(m.bar + b, (unsigned)((ncol * G::KPAD + BLOB) * sizeof(double)));
+          bulk_g2s(ob, r.blobs + (int64_t)cls * BLOB, BLOB * sizeof(double), m.bar + b);
+        }
         __syncwarp();
         for (int c = h; c < ncol; c += 32)
-          bulk_g2s(xb + c * S, a.Mt + (int64_t)m.srcs[b * NC + c] * G::KPAD, G::KPAD * sizeof(double), m.bar + b);
+          bulk_g2s(xb + col_base(c, S), a.Mt + (int64_t)m.srcs[b * NC + c] * G::KPAD, G::KPAD * sizeof(double),
+                   m.bar + b);
       }
       // padding columns of the last n-tile: zeros
       const int ncol8 = (ncol + 7) & ~7;
-      for (int e = h; e < (ncol8 - ncol) * G::KPAD; e += nhelp_t) xb[(ncol + e / G::KPAD) * S + e % G::KPAD] = 0.0;
-      mbar_wait(m.bar + b, parity);
+      for (int e = h; e < (ncol8 - ncol) * G::KPAD; e += nhelp_t)
+        xb[col_base(ncol + e / G::KPAD, S) + e % G::KPAD] = 0.0;
+      if (!(dbg & 8)) mbar_wait(m.bar + b, parity);
+      if (dbg & 2) return;
       // X[col] <- Az_M (D^M_g)^-1 X[col], item = (column, (n, m) pair)
-      const double2* azb = m.azs + b * (P + 1);
       for (int it = h; it < ncol * NCOEF; it += nhelp_t) {
         const int col = it / NCOEF, q = it - col * NCOEF;
-        const int pe = m.pairtab[q], n2 = pe & 0xffff, mm = pe >> 16;
-        const int32_t* sy = m.sym + (m.meta[b * NC + col] >> 8) * 2 * NR;
-        double* xcol = xb + col * S;
+        const int pe = m.pairtab[q], n = pe & 0xffff, mm = pe >> 16;
+        const int g2 = 2 * (m.meta[b * NC + col] >> 8);
+        double* xcol = xb + col_base(col, S);
         if (mm == 0) {
-          const int ent = sy[n2];
-          const double v = xcol[ent & 0xffff];
-          xcol[n2] = (ent >> 16) ? -v : v;
+          if ((m.mmask[q] >> g2) & 2) xcol[q] = -xcol[q];
         } else {
-          const int rre = n2 + 2 * mm - 1, rim = rre + 1;
-          const int e0 = sy[rre], e1 = sy[rim];
-          double u0 = xcol[e0 & 0xffff], u1 = xcol[e1 & 0xffff];
-          u0 = (e0 >> 16) ? -u0 : u0;
-          u1 = (e1 >> 16) ? -u1 : u1;
-          const double2 cs = azb[mm];
-          xcol[rre] = cs.x * u0 - cs.y * u1;
-          xcol[rim] = cs.y * u0 + cs.x * u1;
+          const int rre = q, rim = NCOEF + q - n - 1;
+          const uint32_t f0 = m.mmask[rre] >> g2, f1 = m.mmask[rim] >> g2;
+          const double v0 = xcol[rre], v1 = xcol[rim];
+          double u0 = (f0 & 1) ? v1 : v0, u1 = (f1 & 1) ? v0 : v1;
+          u0 = (f0 & 2) ? -u0 : u0;
+          u1 = (f1 & 2) ? -u1 : u1;
+          const double cs = ob[2 * mm], sn = ob[2 * mm + 1];
+          xcol[rre] = cs * u0 - sn * u1;
+          xcol[rim] = sn * u0 + cs * u1;
         }
       }
     };
     // add chunk ch (buffer b) into the accumulators: acc[slot][r] += (D^L_g Az_L Y)[r]
     auto accumulate = [&](int ch, int b) {
       const double* y = b ? m.x1 : m.x0;
+      const double* ob = m.ob + b * BLOB;
       const int ns = a.chunk_seg[ch + 1] - a.chunk_seg[ch];
       const int* meta = m.meta + b * NC;
       const int* sb = m.sbeg + b * (NC + 1);
       const int* ss = m.sslot + b * NC;
-      const double2* azb = m.azs + b * (P + 1);
       const int RG = max(1, nhelp_t / NR);
       for (int t = h; t < RG * NR; t += nhelp_t) {
         const int rg = t / NR, row = t - rg * NR;
         const int d = m.dec[row], part = d & 1, n = (d >> 1) & 0x7f;
         const int mm = (d >> 8) - cidx(n, 0);
-        const int rre = real_index(n, mm, 0), rim = mm ? rre + 1 : rre;
-        const double2 cs = mm ? azb[mm] : make_double2(1.0, 0.0);
-        const uint32_t mask = (uint32_t)m.lmask[row];
-        // value for (take partner, negate) combinations: src part = part ^ partner
-        const double ca = cs.x, sa = cs.y;
+        const int rre = d >> 8, rim = mm ? NCOEF + rre - n - 1 : rre;
+        const double ca = mm ? ob[2 * mm] : 1.0, sa = mm ? ob[2 * mm + 1] : 0.0;
+        const uint32_t mask = m.lmask[row];
         const int s_lo = ns * rg / RG, s_hi = ns * (rg + 1) / RG;
         for (int sgi = s_lo; sgi < s_hi; ++sgi) {
           double* ap = m.acc + ss[sgi] * NR + row;
           double v = *ap;
           for (int col = sb[sgi]; col < sb[sgi + 1]; ++col) {
             const uint32_t mg = mask >> (2 * (meta[col] >> 8));
-            const double yr = y[col * S + rre], yi = y[col * S + rim];
-            const int src = part ^ (int)(mg & 1);
-            double t0 = src == 0 ? fma(-sa, yi, ca * yr) : fma(ca, yi, sa * yr);
-            if (mm == 0) t0 = yr;
+            const double* yc = y + col_base(col, S);
+            const double yr = yc[rre], yi = yc[rim];
+            const int src = part ^ (int)(mg & 1);  // component of Az_L Y feeding this row
+            const double t0 = src == 0 ? fma(-sa, yi, ca * yr) : fma(ca, yi, sa * yr);
             v += (mg & 2) ? -t0 : t0;
           }
           *ap = v;
@@ -526,7 +536,7 @@ __global__ void __launch_bounds__(512, 1) m2l_rot_kernel(const RotArgs r, int nh
         named_arrive(1 + nb, nall);  // Xfull(i+1)
       }
       named_sync(3 + b, nall);  // Yfull(i)
-      accumulate(ch, b);
+      if (!(dbg & 4)) accumulate(ch, b);
       named_sync(6, nhelp_t);  // helpers done with meta[b] / Y(i) before they are overwritten
     }
   } else {
@@ -535,15 +545,14 @@ __global__ void __launch_bounds__(512, 1) m2l_rot_kernel(const RotArgs r, int nh
       const int i = ch - c_first, b = i & 1;
       named_sync(1 + b, nall);  // Xfull(i)
       double* xc = b ? m.x1 : m.x0;
-      const int cls = a.chunk_class[ch];
+      const double* ob = m.ob + b * BLOB;
       const int ntiles = (a.chunk_begin[ch + 1] - a.chunk_begin[ch] + 7) >> 3;
-      const double* ops = r.rops + (int64_t)cls * rot_ops_size(P);
       for (int st = 0; st < 3; ++st) {
         const int32_t* sl = m.sched + (st * G::NMMA + warp) * r.smax;
-        for (int k = 0; k < r.smax; ++k) {
+        for (int k = 0; k < r.smax && !(dbg & 1); ++k) {
           const int item = sl[k];
           if (item < 0) break;
-          rot_item<P>(ops, m.blkoff, st, item & 0x1f, (item >> 5) & 1, (item >> 6) & 1, ntiles, xc, lane);
+          rot_item<P>(ob, m.blkoff, st, item & 0x1f, (item >> 5) & 1, ntiles, xc, lane);
         }
         if (st < 2) named_sync(5, nmma_t);  // stage st complete before st + 1 reads it
       }
@@ -560,6 +569,31 @@ __global__ void __launch_bounds__(512, 1) m2l_rot_kernel(const RotArgs r, int nh
     const double v = m.acc[e] * a.hpow[a.level[cell] * (a.p + 2) + ((d >> 1) & 0x7f) + 1];
     ((double*)(a.L + (int64_t)cell * a.nc))[2 * (d >> 8) + (d & 1)] = v;
   }
+}
+
+// S9 pre-pass (v3): M~ rows in the RI layout, M~[c][q] = {Re,Im} M_n^m(c) h_c^{-n}, zero for q >= NR.
+__global__ void mtilde_ri_kernel(const double2* __restrict__ M, const int32_t* __restrict__ level,
+                                 const double* __restrict__ hpow, int64_t ncells, int p, int nc, int NR, int Kpad,
+                                 double* __restrict__ Mt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ncells * Kpad) return;
+  const int64_t c = e / Kpad;
+  const int q = (int)(e - c * Kpad);
+  double v = 0.0;
+  if (q < NR) {
+    const int part = q >= nc;
+    const int ci = part ? q - nc + 1 : q;  // Im plane: (n, m >= 1) -> cidx(n, m) = q - nc + n + 1
+    int n = 0;
+    if (part) {
+      while ((n + 1) * n / 2 <= q - nc) ++n;
+    } else {
+      while ((n + 1) * (n + 2) / 2 <= q) ++n;
+    }
+    const int cix = part ? ci + n : ci;
+    const double2 z = M[c * nc + cix];
+    v = (part ? z.y : z.x) * hpow[level[c] * (p + 2) + n];
+  }
+  Mt[e] = v;
 }
 
 // Gauss-Legendre nodes and weights on [-1, 1] (Newton on P_k, host, double)
@@ -616,8 +650,25 @@ void m2l_rot_setup(fmm_plan_s& P) {
   Rs.alloc((int64_t)np * ncoef(p));
   quad_points_kernel<<<cdiv(np * (p + 1), 128), 128, 0, s>>>(dgx, p, Rs);
   FMM_LAUNCHED("quad_points_kernel");
-  D.rot_ops.alloc(D.nclass * rot_ops_size(p));
-  D.rot_az.alloc(D.nclass * (p + 1));
+  D.rot_ops.alloc(D.nclass * rot_blob_size(p));
+  {  // symmetry masks from the signed-permutation tables (m2l_dmma.cu)
+    const int NR = (p + 1) * (p + 1);
+    std::vector<int32_t> sym = build_symtab(p);
+    std::vector<uint32_t> mk(2 * NR, 0);
+    for (int which = 0; which < 2; ++which)
+      for (int q = 0; q < NR; ++q) {  // RI row q <-> real index rr
+        int n, mm, part;
+        ri_decode(p, q, n, mm, part);
+        const int rr = real_index(n, mm, part);
+        for (int g = 0; g < 16; ++g) {
+          const int ent = sym[(g * 2 + which) * NR + rr];
+          if ((ent & 0xffff) != rr) mk[which * NR + q] |= 1u << (2 * g);
+          if (ent >> 16) mk[which * NR + q] |= 2u << (2 * g);
+        }
+      }
+    D.rot_masks.alloc(2 * NR);
+    FMM_CUDA(cudaMemcpyAsync(D.rot_masks.ptr, mk.data(), sizeof(uint32_t) * mk.size(), cudaMemcpyHostToDevice, s));
+  }
   int nent = 0;
   for (int n = 0; n <= p; ++n) nent += (n + 1) * (n + 1) + n * n;
   const size_t sh = sizeof(double2) * kQuadBatch * ncoef(p) + sizeof(double) * nent;
@@ -626,8 +677,7 @@ void m2l_rot_setup(fmm_plan_s& P) {
     FMM_CUDA(cudaFuncSetAttribute(build_rot_ops_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     configured = sh;
   }
-  build_rot_ops_kernel<<<(unsigned)D.nclass, kRotBuildThreads, sh, s>>>(D.class_keys, p, dgx, dgw, Rs, D.rot_ops,
-                                                                         D.rot_az);
+  build_rot_ops_kernel<<<(unsigned)D.nclass, kRotBuildThreads, sh, s>>>(D.class_keys, p, dgx, dgw, Rs, D.rot_ops);
   FMM_LAUNCHED("build_rot_ops_kernel");
   // static LPT schedule of the items of each stage over the MMA warps (full 64-column chunk costs)
   const int nmma = 8;
@@ -635,14 +685,9 @@ void m2l_rot_setup(fmm_plan_s& P) {
   for (int st = 0; st < 3; ++st) {
     std::vector<std::pair<int, int>> items;  // (cost, code)
     for (int blk = 0; blk <= p; ++blk) {
-      const int R = rot_block_rows(p, st, blk), cost1 = ((R + 7) / 8) * ((R + 3) / 4) * 4;
-      const int nparts = rot_block_parts(st, blk);
-      for (int cg = 0; cg < 2; ++cg) {
-        if (st == 1)
-          items.push_back({cost1 * (blk > 0 ? 2 : 1), blk | (cg << 6)});
-        else
-          for (int pt = 0; pt < nparts; ++pt) items.push_back({cost1, blk | (pt << 5) | (cg << 6)});
-      }
+      const int R = rot_block_rows(p, st, blk), cost = ((R + 7) / 8) * ((R + 3) / 4) * 8 + 12;
+      const int nparts = st == 1 ? (blk > 0 ? 2 : 1) : rot_block_parts(st, blk);
+      for (int pt = 0; pt < nparts; ++pt) items.push_back({cost, blk | (pt << 5)});
     }
     std::stable_sort(items.begin(), items.end(), [](auto& x, auto& y) { return x.first > y.first; });
     std::vector<int> load(nmma, 0);
@@ -664,18 +709,27 @@ void m2l_rot_setup(fmm_plan_s& P) {
   FMM_CUDA(cudaStreamSynchronize(s));
 }
 
+void m2l_rot_mtilde(fmm_plan_s& P) {
+  M2LDmma& D = P.m2l_dmma;
+  const int64_t ne = P.cells.n * D.Kpad;
+  mtilde_ri_kernel<<<cdiv(ne, 256), 256, 0, P.stream>>>(P.M, P.cells.level, D.hpow, P.cells.n, P.p, P.nc, D.NR, D.Kpad,
+                                                        D.Mt);
+  FMM_LAUNCHED("mtilde_ri_kernel");
+}
+
 void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
   M2LDmma& D = P.m2l_dmma;
   RotArgs r;
   r.a = a;
-  r.rops = D.rot_ops;
-  r.raz = D.rot_az;
+  r.blobs = D.rot_ops;
+  r.masks = D.rot_masks;
   r.sched = D.rot_sched;
   r.smax = D.rot_smax;
-  r.S = rot_xstride((a.NR + 3) & ~3);
   const size_t sh = rot_smem_bytes(P.p, a.T, D.rot_smax);
   const int nhelp = 8;
-  void (*k)(const RotArgs, int) = nullptr;
+  void (*k)(const RotArgs, int, int) = nullptr;
+  const char* dbgs = getenv("FMM_M2L_DEBUG");  // timing experiments only (skips work: wrong results)
+  const int dbg = dbgs ? atoi(dbgs) : 0;
   switch (P.p) {
     case 5: k = m2l_rot_kernel<5>; break;
     case 6: k = m2l_rot_kernel<6>; break;
@@ -693,7 +747,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
     FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     configured[P.p] = sh;
   }
-  k<<<(unsigned)D.ntiles, 32 * (8 + nhelp), sh, P.stream>>>(r, nhelp);
+  k<<<(unsigned)D.ntiles, 32 * (8 + nhelp), sh, P.stream>>>(r, nhelp, dbg);
   FMM_LAUNCHED("m2l_rot_kernel");
 }
 

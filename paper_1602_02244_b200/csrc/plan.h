@@ -87,14 +87,14 @@ struct M2LDmma {
   DevBuf<double> hpow;         // [22][p + 2]
   DevBuf<uint64_t> class_keys; // [nclass] canonical (level difference, offset) keys
   // M2L v3 (m2l_rot.cu): rotation-factored class operators
-  DevBuf<double> rot_ops;      // [nclass][rot_ops_size(p)] A fragments of the D, Z~, Dt stages
-  DevBuf<double2> rot_az;      // [nclass][p + 1] (cos m alpha, sin m alpha)
+  DevBuf<double> rot_ops;      // [nclass][rot_blob_size(p)] azimuths, D and Z~ blocks per class
+  DevBuf<uint32_t> rot_masks;  // [2][NR] symmetry masks (multipole side, local side)
   DevBuf<int32_t> rot_sched;   // [3][8][rot_smax] MMA-warp item lists
   int rot_smax = 0, rot_T = 0;
   int64_t bytes() const {
     return ops.bytes() + col_src.bytes() + col_meta.bytes() + chunk_begin.bytes() + chunk_class.bytes() +
            tile_chunk.bytes() + tile_cells.bytes() + symtab.bytes() + hpow.bytes() + chunk_seg.bytes() +
-           seg_begin.bytes() + Mt.bytes() + class_keys.bytes() + rot_ops.bytes() + rot_az.bytes() +
+           seg_begin.bytes() + Mt.bytes() + class_keys.bytes() + rot_ops.bytes() + rot_masks.bytes() +
            rot_sched.bytes();
   }
 };

@@ -263,7 +263,8 @@ struct RGeo {
   static constexpr int KPAD = (NR + 3) & ~3;
   static constexpr int S = rot_xstride(KPAD);  // column stride (see col_base)
   static constexpr int NC = 2 * S * 64 * 8 > 140 * 1024 ? 32 : 64;  // as v2's chunk width rule
-  static constexpr int NMMA = 8;
+  static constexpr int NMMA = 16;  // DMMA issue: one per ~66 cycles per warp, one per 16 per SMSP
+  static constexpr int NPREP = 4, NACC = 4;
   static constexpr int MTMAX = (P + 1 + 7) / 8;
   static constexpr int KSMAX = (P + 1 + 3) / 4;
   static constexpr int NCOEF = (P + 1) * (P + 2) / 2;
@@ -272,7 +273,7 @@ struct RGeo {
 struct RotSmem {
   double *acc, *x0, *x1, *ob;  // ob: [2][blob] class data of the chunk in each buffer
   uint64_t* bar;               // [2]
-  int32_t *meta, *srcs, *sslot, *sbeg, *dec, *pairtab, *sched, *blkoff;
+  int32_t *meta, *srcs, *sslot, *sbeg, *dec, *pairtab, *sched, *blkoff, *ncs;
   uint32_t *mmask, *lmask;     // [NR] symmetry masks (bit 2g: take re/im partner, 2g+1: negate)
 };
 template <int P>
@@ -294,7 +295,8 @@ __device__ __forceinline__ RotSmem rot_carve(double* sm, const RotArgs& r) {
   m.lmask = m.mmask + G::NR;
   m.pairtab = (int32_t*)(m.lmask + G::NR);
   m.blkoff = m.pairtab + G::NCOEF;      // [3][P+1][2]
-  m.sched = m.blkoff + 6 * (P + 1);
+  m.ncs = m.blkoff + 6 * (P + 1);  // [2][2] per buffer: columns, slot segments
+  m.sched = m.ncs + 4;
   return m;
 }
 }  // namespace
@@ -302,7 +304,7 @@ size_t rot_smem_bytes(int p, int T, int smax) {
   const int NR = (p + 1) * (p + 1), KPAD = (NR + 3) & ~3, S = rot_xstride(KPAD), nc = ncoef(p);
   const int NC = 2 * S * 64 * 8 > 140 * 1024 ? 32 : 64;
   return sizeof(double) * ((size_t)T * NR + 2 * NC * (size_t)S + 2 * (size_t)rot_blob_size(p)) +
-         sizeof(uint64_t) * 2 + sizeof(int32_t) * (8 * NC + 2 + 3 * NR + nc + 6 * (p + 1) + 3 * 8 * smax);
+         sizeof(uint64_t) * 2 + sizeof(int32_t) * (8 * NC + 2 + 3 * NR + nc + 6 * (p + 1) + 4 + 3 * 16 * smax);
 }
 int rot_chunk_width(int p) {
   const int NR = (p + 1) * (p + 1), KPAD = (NR + 3) & ~3, S = rot_xstride(KPAD);
@@ -339,14 +341,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// One MMA item: block (st, blk), part, all n-tiles of the chunk, in place: the B operand
-// is streamed per k-step, the results stay in registers until every k-step has been read;
-// A operand from the chunk's class data in shared memory.
+// One MMA item: block (st, blk), part pt, n-tiles [t0, t0 + nti) (nti <= 4) of the chunk,
+// in place: the B operand is streamed per k-step, the results stay in registers until every
+// k-step has been read; A operand from the chunk's class data in shared memory.
 template <int P>
-__device__ __forceinline__ void rot_item(const double* ob, const int32_t* blkoff, int st, int blk, int pt,
-                                         int ntiles, double* xc, int lane) {
+__device__ __forceinline__ void rot_item(const double* ob, const int32_t* blkoff, int st, int blk, int pt, int t0,
+                                         int t1, double* xc, int lane) {
   using G = RGeo<P>;
-  constexpr int NT = G::NC / 8;
+  constexpr int NTI = 4;
   const int R = rot_block_rows(P, st, blk), MT = (R + 7) / 8, KS = (R + 3) / 4;
   const double* A = ob + blkoff[(st * (P + 1) + blk) * 2 + (st == 1 ? 0 : pt)];
   const int colb = lane >> 2, kl = lane & 3;
@@ -367,25 +369,26 @@ __device__ __forceinline__ void rot_item(const double* ob, const int32_t* blkoff
       }
       a[mt][ks] = v;
     }
-  double c[G::MTMAX][NT][2];
+  double c[G::MTMAX][NTI][2];
 #pragma unroll
   for (int mt = 0; mt < G::MTMAX; ++mt)
 #pragma unroll
-    for (int t = 0; t < NT; ++t) c[mt][t][0] = c[mt][t][1] = 0.0;
-  const double* xb = xc + col_base(colb, G::S);
+    for (int t = 0; t < NTI; ++t) c[mt][t][0] = c[mt][t][1] = 0.0;
+  const double* xb = xc + col_base(colb, G::S) + 8 * t0 * G::S;
+  const int nt = t1 - t0;
 #pragma unroll
   for (int ks = 0; ks < G::KSMAX; ++ks) {
     if (ks < KS) {
       const int pos = rot_pos(P, st, blk, pt, 4 * ks + kl);
-      double b[NT];
+      double b[NTI];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) b[t] = (t < ntiles && pos >= 0) ? xb[8 * t * G::S + pos] : 0.0;
+      for (int t = 0; t < NTI; ++t) b[t] = (t < nt && pos >= 0) ? xb[8 * t * G::S + pos] : 0.0;
 #pragma unroll
       for (int mt = 0; mt < G::MTMAX; ++mt)
         if (mt < MT)
 #pragma unroll
-          for (int t = 0; t < NT; ++t)
-            if (t < ntiles) dmma884(c[mt][t][0], c[mt][t][1], a[mt][ks], b[t]);
+          for (int t = 0; t < NTI; ++t)
+            if (t < nt) dmma884(c[mt][t][0], c[mt][t][1], a[mt][ks], b[t]);
     }
   }
   __syncwarp();  // every lane's B loads precede the in-place stores
@@ -395,28 +398,30 @@ __device__ __forceinline__ void rot_item(const double* ob, const int32_t* blkoff
     const int r = 8 * mt + colb;
     const int pos = (mt < MT && r < R) ? rot_pos(P, st, blk, pt, r) : -1;
     if (pos < 0) continue;
-    double* y0 = xc + col_base(2 * kl, G::S) + pos;
-    double* y1 = xc + col_base(2 * kl + 1, G::S) + pos;
+    double* y0 = xc + col_base(2 * kl, G::S) + 8 * t0 * G::S + pos;
+    double* y1 = xc + col_base(2 * kl + 1, G::S) + 8 * t0 * G::S + pos;
 #pragma unroll
-    for (int t = 0; t < NT; ++t)
-      if (t < ntiles) {
+    for (int t = 0; t < NTI; ++t)
+      if (t < nt) {
         y0[8 * t * G::S] = sgn * c[mt][t][0];
         y1[8 * t * G::S] = sgn * c[mt][t][1];
       }
   }
 }
 
+// Named barriers: 1/2 Xfull(b) prep -> MMA; 3/4 Yfull(b) MMA -> acc; 7/8 Xfree(b) acc -> prep;
+// 5 MMA warps (between stages); 6 prep warps; 9 acc warps.
 template <int P>
-__global__ void __launch_bounds__(512, 1) m2l_rot_kernel(const RotArgs r, int nhelp, int dbg) {
+__global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>::NACC), 1)
+    m2l_rot_kernel(const RotArgs r, int dbg) {
   using G = RGeo<P>;
   constexpr int NR = G::NR, NC = G::NC, S = G::S, NCOEF = G::NCOEF, BLOB = rot_blob_size(P);
+  constexpr int nmma_t = 32 * G::NMMA, nprep_t = 32 * G::NPREP, nacc_t = 32 * G::NACC;
   extern __shared__ double sm[];
   const RotSmem m = rot_carve<P>(sm, r);
   const M2LArgs& a = r.a;
   const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int tile = blockIdx.x;
-  constexpr int nmma_t = 32 * G::NMMA;
-  const int nhelp_t = 32 * nhelp, nall = nmma_t + nhelp_t;
   // ---- shared tables
   for (int e = tid; e < a.T * NR; e += nthr) m.acc[e] = 0.0;
   for (int q = tid; q < NCOEF; q += nthr) {
@@ -443,18 +448,58 @@ __global__ void __launch_bounds__(512, 1) m2l_rot_kernel(const RotArgs r, int nh
   }
   const int c_first = a.tile_chunk[tile], c_last = a.tile_chunk[tile + 1];
   __syncthreads();
-  if (warp >= G::NMMA) {
-    // ================= helper warps
+  if (warp >= G::NMMA + G::NPREP) {
+    // ================= accumulate warps: acc[slot][r] += (D^L_g Az_L Y)[r] for chunk i
+    const int h = tid - nmma_t - nprep_t;
+    for (int ch = c_first; ch < c_last; ++ch) {
+      const int i = ch - c_first, b = i & 1;
+      named_sync(3 + b, nmma_t + nacc_t);  // Yfull(i)
+      if (!(dbg & 4)) {
+        const double* y = b ? m.x1 : m.x0;
+        const double* ob = m.ob + b * BLOB;
+        const int ns = m.ncs[2 * b + 1];
+        const int* meta = m.meta + b * NC;
+        const int* sb = m.sbeg + b * (NC + 1);
+        const int* ss = m.sslot + b * NC;
+        for (int row = h; row < NR; row += nacc_t) {
+          const int d = m.dec[row], part = d & 1, n = (d >> 1) & 0x7f;
+          const int mm = (d >> 8) - cidx(n, 0);
+          const int rre = d >> 8, rim = mm ? NCOEF + rre - n - 1 : rre;
+          const double ca = mm ? ob[2 * mm] : 1.0, sa = mm ? ob[2 * mm + 1] : 0.0;
+          const uint32_t mask = m.lmask[row];
+          for (int sgi = 0; sgi < ns; ++sgi) {
+            double* ap = m.acc + ss[sgi] * NR + row;
+            double v = *ap;
+            for (int col = sb[sgi]; col < sb[sgi + 1]; ++col) {
+              const uint32_t mg = mask >> (2 * (meta[col] >> 8));
+              const double* yc = y + col_base(col, S);
+              const double yr = yc[rre], yi = yc[rim];
+              const int src = part ^ (int)(mg & 1);  // component of Az_L Y feeding this row
+              const double t0 = src == 0 ? fma(-sa, yi, ca * yr) : fma(ca, yi, sa * yr);
+              v += (mg & 2) ? -t0 : t0;
+            }
+            *ap = v;
+          }
+        }
+      }
+      named_arrive(7 + b, nacc_t + nprep_t);  // Xfree(i): buffer b may take chunk i + 2
+    }
+  } else if (warp >= G::NMMA) {
+    // ================= prep warps: metadata, TMA bulk copies, symmetry map + Az_M in place
     const int h = tid - nmma_t;
-    // stage chunk ch into buffer b: metadata; TMA bulk copies of the class data and of the
-    // source multipoles; then the column's symmetry map and Az_M in place
-    auto prep = [&](int ch, int b, unsigned parity) {
+    for (int ch = c_first; ch < c_last; ++ch) {
+      const int i = ch - c_first, b = i & 1;
+      if (i >= 2) named_sync(7 + b, nacc_t + nprep_t);  // Xfree(i - 2)
       double* xb = b ? m.x1 : m.x0;
       double* ob = m.ob + b * BLOB;
-      load_meta_dev(a, ch, m.meta + b * NC, m.srcs + b * NC, m.sslot + b * NC, m.sbeg + b * (NC + 1), h, nhelp_t);
+      load_meta_dev(a, ch, m.meta + b * NC, m.srcs + b * NC, m.sslot + b * NC, m.sbeg + b * (NC + 1), h, nprep_t);
       const int cls = a.chunk_class[ch];
       const int ncol = a.chunk_begin[ch + 1] - a.chunk_begin[ch];
-      named_sync(6, nhelp_t);  // metadata visible to all helpers
+      if (h == 0) {
+        m.ncs[2 * b] = ncol;
+        m.ncs[2 * b + 1] = a.chunk_seg[ch + 1] - a.chunk_seg[ch];
+      }
+      named_sync(6, nprep_t);  // metadata visible to the prep warps
       if (h < 32 && !(dbg & 8)) {
         fence_proxy_async();  // earlier generic accesses of xb / ob before the async-proxy writes
         if (h == 0) {
@@ -466,97 +511,53 @@ __global__ void __launch_bounds__(512, 1) m2l_rot_kernel(const RotArgs r, int nh
           bulk_g2s(xb + col_base(c, S), a.Mt + (int64_t)m.srcs[b * NC + c] * G::KPAD, G::KPAD * sizeof(double),
                    m.bar + b);
       }
-      // padding columns of the last n-tile: zeros
-      const int ncol8 = (ncol + 7) & ~7;
-      for (int e = h; e < (ncol8 - ncol) * G::KPAD; e += nhelp_t)
+      const int ncol8 = (ncol + 7) & ~7;  // padding columns of the last n-tile: zeros
+      for (int e = h; e < (ncol8 - ncol) * G::KPAD; e += nprep_t)
         xb[col_base(ncol + e / G::KPAD, S) + e % G::KPAD] = 0.0;
-      if (!(dbg & 8)) mbar_wait(m.bar + b, parity);
-      if (dbg & 2) return;
-      // X[col] <- Az_M (D^M_g)^-1 X[col], item = (column, (n, m) pair)
-      for (int it = h; it < ncol * NCOEF; it += nhelp_t) {
-        const int col = it / NCOEF, q = it - col * NCOEF;
-        const int pe = m.pairtab[q], n = pe & 0xffff, mm = pe >> 16;
-        const int g2 = 2 * (m.meta[b * NC + col] >> 8);
-        double* xcol = xb + col_base(col, S);
-        if (mm == 0) {
-          if ((m.mmask[q] >> g2) & 2) xcol[q] = -xcol[q];
-        } else {
-          const int rre = q, rim = NCOEF + q - n - 1;
-          const uint32_t f0 = m.mmask[rre] >> g2, f1 = m.mmask[rim] >> g2;
-          const double v0 = xcol[rre], v1 = xcol[rim];
-          double u0 = (f0 & 1) ? v1 : v0, u1 = (f1 & 1) ? v0 : v1;
-          u0 = (f0 & 2) ? -u0 : u0;
-          u1 = (f1 & 2) ? -u1 : u1;
-          const double cs = ob[2 * mm], sn = ob[2 * mm + 1];
-          xcol[rre] = cs * u0 - sn * u1;
-          xcol[rim] = sn * u0 + cs * u1;
-        }
-      }
-    };
-    // add chunk ch (buffer b) into the accumulators: acc[slot][r] += (D^L_g Az_L Y)[r]
-    auto accumulate = [&](int ch, int b) {
-      const double* y = b ? m.x1 : m.x0;
-      const double* ob = m.ob + b * BLOB;
-      const int ns = a.chunk_seg[ch + 1] - a.chunk_seg[ch];
-      const int* meta = m.meta + b * NC;
-      const int* sb = m.sbeg + b * (NC + 1);
-      const int* ss = m.sslot + b * NC;
-      const int RG = max(1, nhelp_t / NR);
-      for (int t = h; t < RG * NR; t += nhelp_t) {
-        const int rg = t / NR, row = t - rg * NR;
-        const int d = m.dec[row], part = d & 1, n = (d >> 1) & 0x7f;
-        const int mm = (d >> 8) - cidx(n, 0);
-        const int rre = d >> 8, rim = mm ? NCOEF + rre - n - 1 : rre;
-        const double ca = mm ? ob[2 * mm] : 1.0, sa = mm ? ob[2 * mm + 1] : 0.0;
-        const uint32_t mask = m.lmask[row];
-        const int s_lo = ns * rg / RG, s_hi = ns * (rg + 1) / RG;
-        for (int sgi = s_lo; sgi < s_hi; ++sgi) {
-          double* ap = m.acc + ss[sgi] * NR + row;
-          double v = *ap;
-          for (int col = sb[sgi]; col < sb[sgi + 1]; ++col) {
-            const uint32_t mg = mask >> (2 * (meta[col] >> 8));
-            const double* yc = y + col_base(col, S);
-            const double yr = yc[rre], yi = yc[rim];
-            const int src = part ^ (int)(mg & 1);  // component of Az_L Y feeding this row
-            const double t0 = src == 0 ? fma(-sa, yi, ca * yr) : fma(ca, yi, sa * yr);
-            v += (mg & 2) ? -t0 : t0;
+      if (!(dbg & 8)) mbar_wait(m.bar + b, (unsigned)((i >> 1) & 1));
+      if (!(dbg & 2)) {
+#pragma unroll 4
+        for (int it = h; it < ncol * NCOEF; it += nprep_t) {
+          const int col = it / NCOEF, q = it - col * NCOEF;
+          const int pe = m.pairtab[q], n = pe & 0xffff, mm = pe >> 16;
+          const int g2 = 2 * (m.meta[b * NC + col] >> 8);
+          double* xcol = xb + col_base(col, S);
+          if (mm == 0) {
+            if ((m.mmask[q] >> g2) & 2) xcol[q] = -xcol[q];
+          } else {
+            const int rre = q, rim = NCOEF + q - n - 1;
+            const uint32_t f0 = m.mmask[rre] >> g2, f1 = m.mmask[rim] >> g2;
+            const double v0 = xcol[rre], v1 = xcol[rim];
+            double u0 = (f0 & 1) ? v1 : v0, u1 = (f1 & 1) ? v0 : v1;
+            u0 = (f0 & 2) ? -u0 : u0;
+            u1 = (f1 & 2) ? -u1 : u1;
+            const double cs = ob[2 * mm], sn = ob[2 * mm + 1];
+            xcol[rre] = cs * u0 - sn * u1;
+            xcol[rim] = sn * u0 + cs * u1;
           }
-          *ap = v;
         }
       }
-    };
-    if (c_first < c_last) {
-      prep(c_first, 0, 0);
-      named_arrive(1, nall);  // Xfull(0)
-    }
-    for (int ch = c_first; ch < c_last; ++ch) {
-      const int i = ch - c_first, b = i & 1, nb = b ^ 1;
-      if (ch + 1 < c_last) {
-        prep(ch + 1, nb, (unsigned)(((i + 1) >> 1) & 1));
-        named_arrive(1 + nb, nall);  // Xfull(i+1)
-      }
-      named_sync(3 + b, nall);  // Yfull(i)
-      if (!(dbg & 4)) accumulate(ch, b);
-      named_sync(6, nhelp_t);  // helpers done with meta[b] / Y(i) before they are overwritten
+      named_arrive(1 + b, nprep_t + nmma_t);  // Xfull(i)
     }
   } else {
-    // ================= MMA warps
+    // ================= MMA warps: the three block-GEMM stages in place
     for (int ch = c_first; ch < c_last; ++ch) {
       const int i = ch - c_first, b = i & 1;
-      named_sync(1 + b, nall);  // Xfull(i)
+      named_sync(1 + b, nprep_t + nmma_t);  // Xfull(i)
       double* xc = b ? m.x1 : m.x0;
       const double* ob = m.ob + b * BLOB;
-      const int ntiles = (a.chunk_begin[ch + 1] - a.chunk_begin[ch] + 7) >> 3;
+      const int ntiles = (m.ncs[2 * b] + 7) >> 3;
       for (int st = 0; st < 3; ++st) {
         const int32_t* sl = m.sched + (st * G::NMMA + warp) * r.smax;
         for (int k = 0; k < r.smax && !(dbg & 1); ++k) {
           const int item = sl[k];
           if (item < 0) break;
-          rot_item<P>(ob, m.blkoff, st, item & 0x1f, (item >> 5) & 1, ntiles, xc, lane);
+          const int t0 = (item >> 6) & 7, t1 = min(ntiles, t0 + ((item >> 9) & 7));
+          if (t0 < t1) rot_item<P>(ob, m.blkoff, st, item & 0x1f, (item >> 5) & 1, t0, t1, xc, lane);
         }
         if (st < 2) named_sync(5, nmma_t);  // stage st complete before st + 1 reads it
       }
-      named_arrive(3 + b, nall);  // Yfull(i)
+      named_arrive(3 + b, nmma_t + nacc_t);  // Yfull(i)
     }
   }
   __syncthreads();
@@ -680,14 +681,17 @@ void m2l_rot_setup(fmm_plan_s& P) {
   build_rot_ops_kernel<<<(unsigned)D.nclass, kRotBuildThreads, sh, s>>>(D.class_keys, p, dgx, dgw, Rs, D.rot_ops);
   FMM_LAUNCHED("build_rot_ops_kernel");
   // static LPT schedule of the items of each stage over the MMA warps (full 64-column chunk costs)
-  const int nmma = 8;
+  const int nmma = 16;
   std::vector<std::vector<int>> lists(3 * nmma);
   for (int st = 0; st < 3; ++st) {
     std::vector<std::pair<int, int>> items;  // (cost, code)
     for (int blk = 0; blk <= p; ++blk) {
-      const int R = rot_block_rows(p, st, blk), cost = ((R + 7) / 8) * ((R + 3) / 4) * 8 + 12;
+      const int R = rot_block_rows(p, st, blk), mk = ((R + 7) / 8) * ((R + 3) / 4);
       const int nparts = st == 1 ? (blk > 0 ? 2 : 1) : rot_block_parts(st, blk);
-      for (int pt = 0; pt < nparts; ++pt) items.push_back({cost, blk | (pt << 5)});
+      const int ntc = rot_chunk_width(p) / 8;  // n-tiles of a full chunk
+      const int nti = std::min(ntc, mk >= 4 ? 2 : 4);  // n-tiles per item: big blocks split finer
+      for (int pt = 0; pt < nparts; ++pt)
+        for (int t0 = 0; t0 < ntc; t0 += nti) items.push_back({mk * nti + 6, blk | (pt << 5) | (t0 << 6) | (nti << 9)});
     }
     std::stable_sort(items.begin(), items.end(), [](auto& x, auto& y) { return x.first > y.first; });
     std::vector<int> load(nmma, 0);
@@ -726,8 +730,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
   r.sched = D.rot_sched;
   r.smax = D.rot_smax;
   const size_t sh = rot_smem_bytes(P.p, a.T, D.rot_smax);
-  const int nhelp = 8;
-  void (*k)(const RotArgs, int, int) = nullptr;
+  void (*k)(const RotArgs, int) = nullptr;
   const char* dbgs = getenv("FMM_M2L_DEBUG");  // timing experiments only (skips work: wrong results)
   const int dbg = dbgs ? atoi(dbgs) : 0;
   switch (P.p) {
@@ -747,7 +750,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
     FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     configured[P.p] = sh;
   }
-  k<<<(unsigned)D.ntiles, 32 * (8 + nhelp), sh, P.stream>>>(r, nhelp, dbg);
+  k<<<(unsigned)D.ntiles, 32 * (16 + 4 + 4), sh, P.stream>>>(r, dbg);
   FMM_LAUNCHED("m2l_rot_kernel");
 }
 

@@ -1,0 +1,62 @@
+// Microbenchmark (measurement only): DMMA.8x8x4 (mma.sync m8n8k4 f64) throughput and
+// dependent-chain latency on one SM and on all SMs, vs warps per SM and independent
+// accumulators per warp. Informs the M2L kernels' warp / accumulator counts.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int C>
+__global__ void dmma_loop(double* out, int iters) {
+  double c0[C], c1[C];
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+#pragma unroll
+  for (int i = 0; i < C; ++i) c0[i] = c1[i] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < C; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c0[i]), "+d"(c1[i]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < C; ++i) s += c0[i] + c1[i];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
+template <int C>
+void run(int blocks, int warps, int iters) {
+  double* o;
+  cudaMalloc(&o, 1024 * sizeof(double));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dmma_loop<C><<<blocks, 32 * warps>>>(o, 10);
+  cudaEventRecord(e0);
+  dmma_loop<C><<<blocks, 32 * warps>>>(o, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  int dev;
+  cudaGetDevice(&dev);
+  int clk;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  const double n = (double)blocks * warps * C * iters;  // DMMAs
+  const double cycles = ms * 1e-3 * clk * 1e3;
+  printf("blocks %4d warps/blk %2d chains %2d: %.3f ms, %.2f TFLOP/s, %.2f cycles per DMMA per SMSP (per-SM view)\n",
+         blocks, warps, C, ms, n * 512 / (ms * 1e-3) / 1e12,
+         cycles / (n / (blocks < 148 ? blocks : 148) / 4));
+  cudaFree(o);
+}
+
+int main() {
+  for (int w : {1, 2, 4, 8, 16}) {
+    run<1>(1, w, 20000);
+    run<2>(1, w, 20000);
+    run<4>(1, w, 10000);
+    run<8>(1, w, 5000);
+  }
+  run<8>(148, 8, 5000);
+  run<8>(148, 16, 5000);
+  run<4>(148, 16, 10000);
+  return 0;
+}

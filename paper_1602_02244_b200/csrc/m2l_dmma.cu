@@ -619,63 +619,83 @@ struct Geo {
   static constexpr int NKS = KPAD / 4;
   static constexpr int NRPAD = (NR + 15) & ~15;
   static constexpr int NMT = NRPAD / 8;
-  static constexpr int NMMA = NMT / 2;
+  // m-tiles per MMA warp: one warp issues at most one DMMA per ~66 cycles (tools/dmma_probe.cu),
+  // so the DMMA pipe (one per 16 cycles per SMSP) needs >= 16 issuing warps per SM
+  static constexpr int MTW = 2;  // (one m-tile per warp with 16 MMA warps measured no faster)
+  static constexpr int NMMA = NMT / MTW;
+  static constexpr int NHELP = MTW == 1 ? 8 : (2 * ((NR + 31) / 32) < 16 - NMMA ? 2 * ((NR + 31) / 32) : 16 - NMMA);
+  static constexpr int THREADS = 32 * (NMMA + NHELP);
   static constexpr int S = ct_xstride(KPAD);
   static constexpr int NC = 2 * S * 64 * 8 > 140 * 1024 ? 32 : 64;
   static constexpr int Q = (KPAD + 31) / 32;
 };
 
-template <int NT, int S, int NKS>
-__device__ __forceinline__ void gemm_ct(double (&c)[2][8][2], const double* __restrict__ A0,
+template <int MTW, int NT, int S, int NKS>
+__device__ __forceinline__ void gemm_ct(double (&c)[MTW][8][2], const double* __restrict__ A0,
                                         const double* __restrict__ xc, int lane) {
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < MTW; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) c[i][j][0] = c[i][j][1] = 0.0;
-  const double* A1 = A0 + NKS * 32;
   constexpr int D = 4;
-  double ra0[D], ra1[D];
+  double ra[MTW][D];
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
-    ra0[d] = d < NKS ? __ldg(A0 + d * 32) : 0.0;
-    ra1[d] = d < NKS ? __ldg(A1 + d * 32) : 0.0;
-  }
+  for (int i = 0; i < MTW; ++i)
+#pragma unroll
+    for (int d = 0; d < D; ++d) ra[i][d] = d < NKS ? __ldg(A0 + (i * NKS + d) * 32) : 0.0;
   const double* bx = xc + (lane >> 2) * S + (lane & 3);
 #pragma unroll
   for (int ks = 0; ks < NKS; ++ks) {
-    const double a0 = ra0[ks % D], a1 = ra1[ks % D];
-    if (ks + D < NKS) {
-      ra0[ks % D] = __ldg(A0 + (ks + D) * 32);
-      ra1[ks % D] = __ldg(A1 + (ks + D) * 32);
+    double av[MTW];
+#pragma unroll
+    for (int i = 0; i < MTW; ++i) {
+      av[i] = ra[i][ks % D];
+      if (ks + D < NKS) ra[i][ks % D] = __ldg(A0 + (i * NKS + ks + D) * 32);
     }
     double bv[NT];
 #pragma unroll
     for (int j = 0; j < NT; ++j) bv[j] = bx[j * 8 * S + 4 * ks];
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      dmma884(c[0][j][0], c[0][j][1], a0, bv[j]);
-      dmma884(c[1][j][0], c[1][j][1], a1, bv[j]);
-    }
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int i = 0; i < MTW; ++i) dmma884(c[i][j][0], c[i][j][1], av[i], bv[j]);
   }
 }
 
-template <int S, int NKS>
-__device__ __forceinline__ void gemm_ct_dispatch(int nta, double (&c)[2][8][2], const double* A0, const double* xc,
+template <int MTW, int S, int NKS>
+__device__ __forceinline__ void gemm_ct_dispatch(int nta, double (&c)[MTW][8][2], const double* A0, const double* xc,
                                                  int lane) {
   switch (nta) {
-    case 1: gemm_ct<1, S, NKS>(c, A0, xc, lane); break;
-    case 2: gemm_ct<2, S, NKS>(c, A0, xc, lane); break;
-    case 3: gemm_ct<3, S, NKS>(c, A0, xc, lane); break;
-    case 4: gemm_ct<4, S, NKS>(c, A0, xc, lane); break;
-    case 5: gemm_ct<5, S, NKS>(c, A0, xc, lane); break;
-    case 6: gemm_ct<6, S, NKS>(c, A0, xc, lane); break;
-    case 7: gemm_ct<7, S, NKS>(c, A0, xc, lane); break;
-    default: gemm_ct<8, S, NKS>(c, A0, xc, lane); break;
+    case 1: gemm_ct<MTW, 1, S, NKS>(c, A0, xc, lane); break;
+    case 2: gemm_ct<MTW, 2, S, NKS>(c, A0, xc, lane); break;
+    case 3: gemm_ct<MTW, 3, S, NKS>(c, A0, xc, lane); break;
+    case 4: gemm_ct<MTW, 4, S, NKS>(c, A0, xc, lane); break;
+    case 5: gemm_ct<MTW, 5, S, NKS>(c, A0, xc, lane); break;
+    case 6: gemm_ct<MTW, 6, S, NKS>(c, A0, xc, lane); break;
+    case 7: gemm_ct<MTW, 7, S, NKS>(c, A0, xc, lane); break;
+    default: gemm_ct<MTW, 8, S, NKS>(c, A0, xc, lane); break;
   }
+}
+
+// Y[col][row] over the consumed X buffer, MTW m-tiles per warp (rows < NR only)
+template <int MTW>
+__device__ __forceinline__ void stage_y_ct(const double (&c)[MTW][8][2], double* xc, int S, int NR, int nta, int warp,
+                                           int lane) {
+#pragma unroll
+  for (int i = 0; i < MTW; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int row = 8 * (MTW * warp + i) + (lane >> 2);
+      const int col = 8 * j + 2 * (lane & 3);
+      if (j < nta && row < NR) {
+        xc[col * S + row] = c[i][j][0];
+        xc[(col + 1) * S + row] = c[i][j][1];
+      }
+    }
 }
 
 template <int P>
-__global__ void __launch_bounds__(512, 1) m2l_ws_ct_kernel(const M2LArgs a, int nhelp) {
+__global__ void __launch_bounds__(Geo<P>::THREADS, 1) m2l_ws_ct_kernel(const M2LArgs a, int nhelp) {
   using G = Geo<P>;
   constexpr int NR = G::NR, NC = G::NC, S = G::S;
   extern __shared__ double sm[];
@@ -717,11 +737,11 @@ __global__ void __launch_bounds__(512, 1) m2l_ws_ct_kernel(const M2LArgs a, int 
       double* xc = b ? m.x1 : m.x0;
       const int cls = a.chunk_class[ch];
       const int nta = (a.chunk_begin[ch + 1] - a.chunk_begin[ch] + 7) >> 3;
-      double c[2][8][2];
-      const double* A0 = a.ops + (((int64_t)cls * G::NMT + 2 * warp) * G::NKS) * 32 + lane;
-      gemm_ct_dispatch<S, G::NKS>(nta, c, A0, xc, lane);
+      double c[G::MTW][8][2];
+      const double* A0 = a.ops + (((int64_t)cls * G::NMT + G::MTW * warp) * G::NKS) * 32 + lane;
+      gemm_ct_dispatch<G::MTW, S, G::NKS>(nta, c, A0, xc, lane);
       named_sync(5, nmma_t);
-      stage_y(c, xc, S, NR, nta, warp, lane);
+      stage_y_ct<G::MTW>(c, xc, S, NR, nta, warp, lane);
       named_arrive(3 + b, nall);
     }
   }
@@ -795,11 +815,17 @@ void m2l_dmma_setup(fmm_plan_s& P) {
   if (2 * (size_t)D.ystride * D.NC * sizeof(double) > 140 * 1024) D.NC = kNC / 2;  // large p: 32-column chunks
   D.T = 64;
   while (D.T > 8 && m2l_smem_bytes(D) > 220 * 1024) D.T /= 2;
-  if (P.m2l_variant == 3 && !(m2l_rot_supported(p) && rot_chunk_width(p) == D.NC)) P.m2l_variant = 2;
-  if (P.m2l_variant == 3) {
+  if (P.m2l_variant == 3 && !m2l_rot_supported(p)) P.m2l_variant = 2;
+  if (P.m2l_variant == 3) {  // v3 chunk width and tile size (shared-memory budget), else v2
     D.T = 64;
-    while (D.T > 8 && rot_smem_bytes(p, D.T, 24) > 225 * 1024) D.T /= 2;
+    while (D.T > 16 && rot_smem_bytes(p, D.T, 8) > 225 * 1024) D.T /= 2;
+    if (rot_smem_bytes(p, D.T, 8) > 225 * 1024)
+      P.m2l_variant = 2, D.T = 64;
+    else
+      D.NC = rot_chunk_width(p);
   }
+  if (P.m2l_variant == 2)
+    while (D.T > 8 && m2l_smem_bytes(D) > 220 * 1024) D.T /= 2;
   // warp-specialised kernel: nmt/2 MMA warps + ceil(NR/32) helper warps, <= 512 threads
   D.nhelp = std::min(2 * ((D.NR + 31) / 32), 16 - D.nmt / 2);
   D.use_ws = D.nhelp >= 1 && D.NR > 32 && D.Kpad <= 256 && getenv("FMM_M2L_NO_WS") == nullptr;
@@ -979,23 +1005,24 @@ void m2l_dmma_pass(fmm_plan_s& P) {
   static size_t configured_ct[16] = {0};
   if (D.use_ws && P.p >= 5 && P.p <= 14 && getenv("FMM_M2L_NO_CT") == nullptr) {
     void (*k)(const M2LArgs, int) = nullptr;
+    int thr = 0, nh = 0;
     switch (P.p) {
-      case 5: k = m2l_ws_ct_kernel<5>; break;
-      case 6: k = m2l_ws_ct_kernel<6>; break;
-      case 7: k = m2l_ws_ct_kernel<7>; break;
-      case 8: k = m2l_ws_ct_kernel<8>; break;
-      case 9: k = m2l_ws_ct_kernel<9>; break;
-      case 10: k = m2l_ws_ct_kernel<10>; break;
-      case 11: k = m2l_ws_ct_kernel<11>; break;
-      case 12: k = m2l_ws_ct_kernel<12>; break;
-      case 13: k = m2l_ws_ct_kernel<13>; break;
-      default: k = m2l_ws_ct_kernel<14>; break;
+      case 5: k = m2l_ws_ct_kernel<5>, thr = Geo<5>::THREADS, nh = Geo<5>::NHELP; break;
+      case 6: k = m2l_ws_ct_kernel<6>, thr = Geo<6>::THREADS, nh = Geo<6>::NHELP; break;
+      case 7: k = m2l_ws_ct_kernel<7>, thr = Geo<7>::THREADS, nh = Geo<7>::NHELP; break;
+      case 8: k = m2l_ws_ct_kernel<8>, thr = Geo<8>::THREADS, nh = Geo<8>::NHELP; break;
+      case 9: k = m2l_ws_ct_kernel<9>, thr = Geo<9>::THREADS, nh = Geo<9>::NHELP; break;
+      case 10: k = m2l_ws_ct_kernel<10>, thr = Geo<10>::THREADS, nh = Geo<10>::NHELP; break;
+      case 11: k = m2l_ws_ct_kernel<11>, thr = Geo<11>::THREADS, nh = Geo<11>::NHELP; break;
+      case 12: k = m2l_ws_ct_kernel<12>, thr = Geo<12>::THREADS, nh = Geo<12>::NHELP; break;
+      case 13: k = m2l_ws_ct_kernel<13>, thr = Geo<13>::THREADS, nh = Geo<13>::NHELP; break;
+      default: k = m2l_ws_ct_kernel<14>, thr = Geo<14>::THREADS, nh = Geo<14>::NHELP; break;
     }
     if (sh > 48 * 1024 && sh > configured_ct[P.p]) {
       FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
       configured_ct[P.p] = sh;
     }
-    k<<<(unsigned)D.ntiles, 32 * (nmma + nhelp), sh, P.stream>>>(a, nhelp);
+    k<<<(unsigned)D.ntiles, thr, sh, P.stream>>>(a, nh);
     FMM_LAUNCHED("m2l_ws_ct_kernel");
     return;
   }

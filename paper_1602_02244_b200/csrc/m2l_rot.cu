@@ -25,18 +25,20 @@
 // Work per pair (p = 10): 3 x 891 useful MACs (1392 padded DMMA-MAC blocks of 8x8x4 per
 // 64 columns) instead of the dense 121^2 = 14641 (3968 DMMAs per 64 columns).
 //
-// Kernel (one CTA per tile of T target cells, as v2): warp-specialised.
-//  * helper warps: load chunk i+1's metadata, stage its source multipoles M~_B (contiguous
-//    rows of Kpad doubles) into shared memory with cp.async.bulk (TMA bulk copies, one per
-//    column, completion on an mbarrier), apply the column's symmetry map and Az_M in place,
-//    signal the MMA warps; then add chunk i's result (Az_L and the symmetry map applied on
-//    the fly) into the tile's shared-memory accumulators (deterministic column order);
-//  * MMA warps: the three block-GEMM stages D, Z~, Dt on DMMA (mma.sync m8n8k4 f64), each
-//    IN PLACE in the chunk's shared-memory buffer: an item = (block, part, half of the
-//    columns) reads and writes only its own positions (all B fragments are loaded into
-//    registers before the first store), a named barrier separates the stages; operator
-//    A fragments are streamed from L2; items are spread over the warps by a static LPT
-//    schedule built on the host.
+// Kernel (one CTA per tile of T target cells, as v2): warp-specialised, 16 warps.
+//  * 4 prep warps: load chunk i's metadata, stage its class data (A fragments, azimuths)
+//    and its source multipoles M~_B (contiguous rows of Kpad doubles) into shared memory
+//    with cp.async.bulk (TMA bulk copies, completion on an mbarrier), apply each column's
+//    symmetry map and Az_M in place, signal the MMA warps;
+//  * 8 MMA warps: the three block-GEMM stages D, Z~, Dt on DMMA (mma.sync m8n8k4 f64), each
+//    IN PLACE in the chunk's shared-memory buffer. The small per-degree / per-order blocks
+//    are packed block-diagonally into "items" of two fixed shapes (16 x 4 KSB, 8 x 8); an
+//    item reads and writes only its own positions (all B fragments are read before the
+//    first store), A fragments come pre-arranged in fragment order (one 256-byte load per
+//    fragment), a named barrier separates the stages, items are spread over the warps by a
+//    static LPT schedule built on the host;
+//  * 4 accumulate warps: add chunk i's result (Az_L and the symmetry map applied on the fly)
+//    into the tile's shared-memory accumulators in column order (deterministic, no atomics).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -49,31 +51,9 @@
 namespace fmm {
 namespace m2l {
 
-// --------------------------------------------------------------------- class data layout
-// One class's data ("blob", doubles): az[p+1] (cos m a, sin m a) | per degree n: D_re (n+1)^2
-// row-major, D_im (n+1)^2 (row/column 0 zero) | per order m: Z~_m (p+1-m)^2 row-major;
-// padded to an even count (16-byte bulk copies). Stage st of block blk reads its A operand
-// from it: st 0 D, st 1 Z~, st 2 D transposed (Re: E^-1 D^T E).
-__host__ __device__ inline int rot_block_rows(int p, int st, int blk) { return st == 1 ? p + 1 - blk : blk + 1; }
-__host__ __device__ inline int rot_block_parts(int st, int blk) { return st == 1 ? 1 : (blk > 0 ? 2 : 1); }
-__host__ __device__ constexpr int rot_d_offset(int p, int n, int part) {
-  int off = 2 * (p + 1);
-  for (int k = 0; k < n; ++k) off += 2 * (k + 1) * (k + 1);
-  return off + part * (n + 1) * (n + 1);
-}
-__host__ __device__ constexpr int rot_z_offset(int p, int m) {
-  int off = rot_d_offset(p, p + 1, 0);
-  for (int k = 0; k < m; ++k) off += (p + 1 - k) * (p + 1 - k);
-  return off;
-}
-__host__ __device__ constexpr int rot_blob_size(int p) { return (rot_z_offset(p, p + 1) + 1) & ~1; }
-__host__ __device__ inline int rot_block_offset(int p, int st, int blk, int part) {
-  return st == 1 ? rot_z_offset(p, blk) : rot_d_offset(p, blk, part);
-}
-
 // "RI" layout of one expansion in the M2L v3 kernel (and of M~ rows): a Re plane
 // (n, m >= 0) at n(n+1)/2 + m followed by an Im plane (n, m >= 1) at nc + n(n-1)/2 + m - 1;
-// (p+1)^2 doubles, and both rotation stages read/write runs contiguous in m.
+// (p+1)^2 doubles; the rotation blocks read and write runs contiguous in m.
 __host__ __device__ inline int ri_pos(int p, int n, int m, int part) {
   return part == 0 ? n * (n + 1) / 2 + m : (p + 1) * (p + 2) / 2 + n * (n - 1) / 2 + m - 1;
 }
@@ -85,19 +65,32 @@ __host__ __device__ inline void ri_decode(int p, int q, int& n, int& m, int& par
   while ((part ? (n + 1) * n / 2 : (n + 1) * (n + 2) / 2) <= q) ++n;
   m = part ? q - n * (n - 1) / 2 + 1 : q - n * (n + 1) / 2;
 }
-// position of row/column index r of block (st, blk, part); -1 = none (zero)
-__host__ __device__ inline int rot_pos(int p, int st, int blk, int part, int r) {
-  if (st == 1) {  // order m = blk, degree n = m + r
-    if (r > p - blk) return -1;
-    return ri_pos(p, blk + r, blk, part);
-  }
-  if (r > blk || (part == 1 && r == 0)) return -1;  // degree n = blk, order m = r
-  return ri_pos(p, blk, r, part);
-}
 // column base in a chunk buffer: stride S (= 4 mod 16 doubles) plus a +-4 swizzle on columns
 // 4..7 of every 8, so B-fragment loads (8 columns x 4 rows) and C-fragment stores (8 rows x
 // columns 2k+e) both hit 16 distinct 8-byte banks per half-warp on contiguous positions
 __host__ __device__ inline int col_base(int c, int S) { return c * S + ((c & 4) ? ((c & 1) ? -4 : 4) : 0); }
+
+constexpr int rot_xstride(int kpad) {
+  int s = kpad + 8;  // room for the +-4 column swizzle
+  while (s % 16 != 4) ++s;
+  return s;
+}
+// chunk width (columns) of the v3 kernel and its shared-memory budget
+constexpr int rot_nc(int p) { return p <= 10 ? 40 : 32; }
+constexpr int rot_ksb(int p) { return (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB)
+// ints of one per-chunk descriptor: [ncol, nseg, class, 0 | srcs | meta | sslot | sbeg[NC + 1]]
+constexpr int rot_desc_ints(int nc) { return (4 + 4 * nc + 1 + 3) & ~3; }
+
+// ------------------------------------------------------------------------- items (host)
+// A block: stage 0/2 = rotation of degree n, part (Re: m = 0..n, Im: m = 1..n); stage 1 =
+// z translation of order m (n = m..p; Re and Im parts share the operator). An item packs
+// blocks block-diagonally into slots 0..15 (big: 16 rows x 4 KSB k, one block of size > 8)
+// or 0..7 (small: 8 x 8); slot s is both row s and k index s.
+struct RotItem {
+  int st, big, nparts, aoff;   // aoff: first double of its fragments in a class blob
+  int slot[16];                // block code (stage 0/2: n | part << 5; stage 1: m) | local << 8, -1 empty
+  int pos[2][16];              // RI position of each slot per part (stage 1: Re, Im), -1 none
+};
 
 }  // namespace m2l
 
@@ -105,7 +98,6 @@ namespace {
 using namespace m2l;
 
 // ------------------------------------------------------------------- setup: operators
-// Regular harmonics at the quadrature points s_i (shared by every class).
 __global__ void quad_points_kernel(const double* __restrict__ glx, int p, double2* __restrict__ Rs) {
   const int nphi = 2 * p + 1, np = (p + 1) * nphi, nc = ncoef(p);
   for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < np * (p + 1); it += gridDim.x * blockDim.x) {
@@ -118,15 +110,22 @@ __global__ void quad_points_kernel(const double* __restrict__ glx, int p, double
   }
 }
 
+
 constexpr int kRotBuildThreads = 256;
 constexpr int kQuadBatch = 32;
 constexpr int kMaxEntPerThread = 13;  // ceil(sum_n (n+1)^2 + n^2 at p = 16 / 256)
 
-// One CTA per class: azimuth table, rotation blocks by quadrature, fragments of the three
-// stages in DMMA A-fragment order (A[8 mt + lane/4][4 ks + lane%4]).
+struct ItemDev {  // device copy of RotItem (setup only)
+  int st, big, nparts, aoff;
+  int slot[16];
+};
+
+// One CTA per class: azimuth table, rotation blocks by quadrature, then every item's A
+// fragments in DMMA fragment order (A[8 mt + lane/4][4 ks + lane%4]).
 __global__ void __launch_bounds__(kRotBuildThreads) build_rot_ops_kernel(
     const uint64_t* __restrict__ class_keys, int p, const double* __restrict__ glx, const double* __restrict__ glw,
-    const double2* __restrict__ Rs, double* __restrict__ blobs) {
+    const double2* __restrict__ Rs, const ItemDev* __restrict__ items, int nitems, int blob,
+    double* __restrict__ blobs) {
   extern __shared__ double2 sh[];  // Rq[kQuadBatch][nc], then D[nent] (doubles)
   const int nc = ncoef(p), nphi = 2 * p + 1, np = (p + 1) * nphi;
   double2* Rq = sh;
@@ -140,7 +139,7 @@ __global__ void __launch_bounds__(kRotBuildThreads) build_rot_ops_kernel(
   const double alpha = atan2(y0, x0), beta = atan2(rxy, z0);
   const double cb = cos(beta), sb = sin(beta);
   const double fA = dl < 0 ? ldexp(1.0, -dl) : 1.0, fB = dl > 0 ? ldexp(1.0, dl) : 1.0;
-  double* out = blobs + (int64_t)cls * rot_blob_size(p);
+  double* out = blobs + (int64_t)cls * blob;
   if (tid <= p) {
     double s, c;
     sincos(tid * alpha, &s, &c);
@@ -214,66 +213,69 @@ __global__ void __launch_bounds__(kRotBuildThreads) build_rot_ops_kernel(
     Dtab[e] = (2.0 * n + 1.0) / nphi * c2 * acc[q];
   }
   __syncthreads();
-  // D blocks (Re, Im with zero row/column 0) and Z~ blocks, row-major
-  for (int n = 0; n <= p; ++n) {
-    int base = 0;  // start of degree n in Dtab
-    for (int k = 0; k < n; ++k) base += (k + 1) * (k + 1) + k * k;
-    const int R = n + 1;
-    for (int e = tid; e < 2 * R * R; e += blockDim.x) {
-      const int part = e / (R * R), rr = (e / R) % R, kk = e % R;
+  // fragments of every item
+  for (int it = 0; it < nitems; ++it) {
+    const ItemDev& I = items[it];
+    const int MT = I.big ? 2 : 1, KS = I.big ? rot_ksb(p) : 2;
+    for (int e = tid; e < MT * KS * 32; e += blockDim.x) {
+      const int lane = e & 31, fr = e >> 5, ks = fr % KS, mt = fr / KS;
+      const int r = 8 * mt + (lane >> 2), k = 4 * ks + (lane & 3);
+      const int sr = r < 16 ? I.slot[r] : -1, sk = k < 16 ? I.slot[k] : -1;
       double v = 0.0;
-      if (part == 0)
-        v = Dtab[base + rr * R + kk];
-      else if (rr > 0 && kk > 0)
-        v = Dtab[base + R * R + (rr - 1) * n + (kk - 1)];
-      out[rot_d_offset(p, n, part) + rr * R + kk] = v;
+      if (sr >= 0 && sk >= 0 && (sr & 0xff) == (sk & 0xff)) {
+        const int lr = sr >> 8, lk = sk >> 8;
+        if (I.st == 1) {  // Z~_m[j][n]: j = m + lr, n = m + lk
+          const int m = sr & 0x1f, j = m + lr, n = m + lk;
+          double g = 1.0 / rho;  // (j+n)! / rho^{j+n+1}
+          for (int l = 1; l <= j + n; ++l) g *= l / rho;
+          for (int t = 0; t <= j; ++t) g *= fA;
+          for (int t = 0; t < n; ++t) g *= fB;
+          v = ((n + m) & 1) ? -g : g;
+        } else {
+          const int n = sr & 0x1f, part = (sr >> 5) & 1;
+          const int mr = part ? lr + 1 : lr, mk = part ? lk + 1 : lk;
+          const int a = I.st == 0 ? mr : mk, b = I.st == 0 ? mk : mr;  // stage 2: transposed
+          int base = 0;
+          for (int q = 0; q < n; ++q) base += (q + 1) * (q + 1) + q * q;
+          v = part ? Dtab[base + (n + 1) * (n + 1) + (a - 1) * n + (b - 1)] : Dtab[base + a * (n + 1) + b];
+          if (I.st == 2 && part == 0) v *= (mk == 0 ? 1.0 : 2.0) / (mr == 0 ? 1.0 : 2.0);  // E^-1 D^T E
+        }
+      }
+      out[I.aoff + e] = v;
     }
   }
-  for (int m = 0; m <= p; ++m) {
-    const int R = p + 1 - m;
-    for (int e = tid; e < R * R; e += blockDim.x) {
-      const int i = e / R, k = e % R, j = m + i, n = m + k;
-      double g = 1.0 / rho;  // (j+n)! / rho^{j+n+1}
-      for (int l = 1; l <= j + n; ++l) g *= l / rho;
-      for (int t = 0; t <= j; ++t) g *= fA;
-      for (int t = 0; t < n; ++t) g *= fB;
-      out[rot_z_offset(p, m) + e] = ((n + m) & 1) ? -g : g;
-    }
-  }
-  if (tid == 0 && (rot_z_offset(p, p + 1) & 1)) out[rot_z_offset(p, p + 1)] = 0.0;
 }
 
 // ------------------------------------------------------------------- the mat-vec kernel
 struct RotArgs {
   M2LArgs a;
-  const double* blobs;   // [nclass][rot_blob_size(p)] class data (azimuths, D and Z~ blocks)
+  const double* blobs;   // [nclass][blob] class data: azimuths | A fragments of every item
   const uint32_t* masks; // [2][NR] symmetry masks: 0 = multipole side (inverse map), 1 = local side
-  const int32_t* sched;  // [3][nmma][smax] items (-1 = end)
-  int smax, S;
+  const int32_t* sched;  // [3][NMMA][smax] item ids (-1 = end)
+  const int32_t* ihdr;   // [nitems] big | nparts << 1 | aoff << 8
+  const int32_t* ipos;   // [nitems][2][16] RI positions
+  const int32_t* desc;   // [nchunks][rot_desc_ints(NC)] chunk descriptors
+  int smax, nitems, blob;
 };
 
-constexpr int rot_xstride(int kpad) {
-  int s = kpad + 8;  // room for the +-4 column swizzle
-  while (s % 16 != 4) ++s;
-  return s;
-}
 template <int P>
 struct RGeo {
   static constexpr int NR = (P + 1) * (P + 1);
   static constexpr int KPAD = (NR + 3) & ~3;
   static constexpr int S = rot_xstride(KPAD);  // column stride (see col_base)
-  static constexpr int NC = 2 * S * 64 * 8 > 140 * 1024 ? 32 : 64;  // as v2's chunk width rule
-  static constexpr int NMMA = 16;  // DMMA issue: one per ~66 cycles per warp, one per 16 per SMSP
-  static constexpr int NPREP = 4, NACC = 4;
-  static constexpr int MTMAX = (P + 1 + 7) / 8;
-  static constexpr int KSMAX = (P + 1 + 3) / 4;
+  static constexpr int NC = rot_nc(P);
+  static constexpr int NT = NC / 8;
+  static constexpr int NMMA = 8, NPREP = 4, NACC = 8;
+  static constexpr int KSB = rot_ksb(P);
   static constexpr int NCOEF = (P + 1) * (P + 2) / 2;
 };
 
 struct RotSmem {
   double *acc, *x0, *x1, *ob;  // ob: [2][blob] class data of the chunk in each buffer
-  uint64_t* bar;               // [2]
-  int32_t *meta, *srcs, *sslot, *sbeg, *dec, *pairtab, *sched, *blkoff, *ncs;
+  uint64_t* bar;               // [2] X + class data of buffer b; [2 + j] descriptor buffer j (0..2)
+  int32_t *desc;               // [3][rot_desc_ints(NC)] chunk descriptors (chunk i in i % 3)
+  int32_t *dec, *pairtab, *sched, *ihdr, *ipos;
+  int2* colt;                  // [2][NC] per buffer: (column base, 2 g) of each chunk column
   uint32_t *mmask, *lmask;     // [NR] symmetry masks (bit 2g: take re/im partner, 2g+1: negate)
 };
 template <int P>
@@ -284,33 +286,19 @@ __device__ __forceinline__ RotSmem rot_carve(double* sm, const RotArgs& r) {
   m.x0 = m.acc + (size_t)r.a.T * G::NR;
   m.x1 = m.x0 + G::NC * G::S;
   m.ob = m.x1 + G::NC * G::S;
-  uint64_t* b = (uint64_t*)(m.ob + 2 * rot_blob_size(P));
+  uint64_t* b = (uint64_t*)(m.ob + 2 * r.blob);
   m.bar = b;
-  m.meta = (int32_t*)(b + 2);
-  m.srcs = m.meta + 2 * G::NC;
-  m.sslot = m.srcs + 2 * G::NC;
-  m.sbeg = m.sslot + 2 * G::NC;
-  m.dec = m.sbeg + 2 * (G::NC + 1);
+  m.desc = (int32_t*)(b + 6);  // 16-byte aligned (ob and bar sizes are multiples of 16)
+  m.dec = m.desc + 3 * rot_desc_ints(G::NC);
   m.mmask = (uint32_t*)(m.dec + G::NR);
   m.lmask = m.mmask + G::NR;
   m.pairtab = (int32_t*)(m.lmask + G::NR);
-  m.blkoff = m.pairtab + G::NCOEF;      // [3][P+1][2]
-  m.ncs = m.blkoff + 6 * (P + 1);  // [2][2] per buffer: columns, slot segments
-  m.sched = m.ncs + 4;
+  m.colt = (int2*)(((uintptr_t)(m.pairtab + G::NCOEF) + 7) & ~(uintptr_t)7);
+  m.ihdr = (int32_t*)(m.colt + 2 * G::NC);
+  m.ipos = m.ihdr + r.nitems;
+  m.sched = m.ipos + 32 * r.nitems;
   return m;
 }
-}  // namespace
-size_t rot_smem_bytes(int p, int T, int smax) {
-  const int NR = (p + 1) * (p + 1), KPAD = (NR + 3) & ~3, S = rot_xstride(KPAD), nc = ncoef(p);
-  const int NC = 2 * S * 64 * 8 > 140 * 1024 ? 32 : 64;
-  return sizeof(double) * ((size_t)T * NR + 2 * NC * (size_t)S + 2 * (size_t)rot_blob_size(p)) +
-         sizeof(uint64_t) * 2 + sizeof(int32_t) * (8 * NC + 2 + 3 * NR + nc + 6 * (p + 1) + 4 + 3 * 16 * smax);
-}
-int rot_chunk_width(int p) {
-  const int NR = (p + 1) * (p + 1), KPAD = (NR + 3) & ~3, S = rot_xstride(KPAD);
-  return 2 * S * 64 * 8 > 140 * 1024 ? 32 : 64;
-}
-namespace {
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
@@ -341,82 +329,83 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// One MMA item: block (st, blk), part pt, n-tiles [t0, t0 + nti) (nti <= 4) of the chunk,
-// in place: the B operand is streamed per k-step, the results stay in registers until every
-// k-step has been read; A operand from the chunk's class data in shared memory.
-template <int P>
-__device__ __forceinline__ void rot_item(const double* ob, const int32_t* blkoff, int st, int blk, int pt, int t0,
-                                         int t1, double* xc, int lane) {
+
+// One MMA item of shape MT x KS (k-steps), NT n-tiles (compile-time), in place: B streamed
+// per k-step, results held in registers until every k-step was read.
+template <int P, int MT, int KS, int NT>
+__device__ __forceinline__ void rot_item_nt(const double* __restrict__ A, const int32_t* pos, int nparts, double sgn1,
+                                            double* xc, int lane, int dbg) {
   using G = RGeo<P>;
-  constexpr int NTI = 4;
-  const int R = rot_block_rows(P, st, blk), MT = (R + 7) / 8, KS = (R + 3) / 4;
-  const double* A = ob + blkoff[(st * (P + 1) + blk) * 2 + (st == 1 ? 0 : pt)];
   const int colb = lane >> 2, kl = lane & 3;
-  double a[G::MTMAX][G::KSMAX];
+  double a[MT][KS];
 #pragma unroll
-  for (int mt = 0; mt < G::MTMAX; ++mt)
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int ks = 0; ks < G::KSMAX; ++ks) {
-      const int rr = 8 * mt + colb, kk = 4 * ks + kl;
-      double v = 0.0;
-      if (mt < MT && ks < KS && rr < R && kk < R) {
-        if (st == 2) {  // transposed; Re: E^-1 D^T E
-          v = A[kk * R + rr];
-          if (pt == 0) v *= (kk == 0 ? 1.0 : 2.0) * (rr == 0 ? 1.0 : 0.5);
-        } else {
-          v = A[rr * R + kk];
-        }
-      }
-      a[mt][ks] = v;
+    for (int ks = 0; ks < KS; ++ks) a[mt][ks] = A[(mt * KS + ks) * 32 + lane];
+  const double* xb = xc + col_base(colb, G::S);
+  for (int pp = 0; pp < nparts; ++pp) {
+    const int32_t* ps = pos + 16 * pp;
+    int qk[KS], qr[MT];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) qk[ks] = 4 * ks + kl < 16 ? ps[4 * ks + kl] : -1;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) qr[mt] = ps[8 * mt + colb];
+    double c[MT][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int t = 0; t < NT; ++t) c[mt][t][0] = c[mt][t][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int q = qk[ks];
+      double b[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) b[t] = (q >= 0 && !(dbg & 64)) ? xb[8 * t * G::S + q] : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dmma884(c[mt][t][0], c[mt][t][1], a[mt][ks], b[t]);
     }
-  double c[G::MTMAX][NTI][2];
+    __syncwarp();  // every lane's B loads precede the in-place stores
+    const double sgn = pp ? sgn1 : 1.0;
 #pragma unroll
-  for (int mt = 0; mt < G::MTMAX; ++mt)
+    for (int mt = 0; mt < MT; ++mt) {
+      const int q = qr[mt];
+      if (q < 0 || (dbg & 32)) continue;
+      double* y0 = xc + col_base(2 * kl, G::S) + q;
+      double* y1 = xc + col_base(2 * kl + 1, G::S) + q;
 #pragma unroll
-    for (int t = 0; t < NTI; ++t) c[mt][t][0] = c[mt][t][1] = 0.0;
-  const double* xb = xc + col_base(colb, G::S) + 8 * t0 * G::S;
-  const int nt = t1 - t0;
-#pragma unroll
-  for (int ks = 0; ks < G::KSMAX; ++ks) {
-    if (ks < KS) {
-      const int pos = rot_pos(P, st, blk, pt, 4 * ks + kl);
-      double b[NTI];
-#pragma unroll
-      for (int t = 0; t < NTI; ++t) b[t] = (t < nt && pos >= 0) ? xb[8 * t * G::S + pos] : 0.0;
-#pragma unroll
-      for (int mt = 0; mt < G::MTMAX; ++mt)
-        if (mt < MT)
-#pragma unroll
-          for (int t = 0; t < NTI; ++t)
-            if (t < nt) dmma884(c[mt][t][0], c[mt][t][1], a[mt][ks], b[t]);
-    }
-  }
-  __syncwarp();  // every lane's B loads precede the in-place stores
-  const double sgn = (st == 1 && pt == 1) ? -1.0 : 1.0;
-#pragma unroll
-  for (int mt = 0; mt < G::MTMAX; ++mt) {
-    const int r = 8 * mt + colb;
-    const int pos = (mt < MT && r < R) ? rot_pos(P, st, blk, pt, r) : -1;
-    if (pos < 0) continue;
-    double* y0 = xc + col_base(2 * kl, G::S) + 8 * t0 * G::S + pos;
-    double* y1 = xc + col_base(2 * kl + 1, G::S) + 8 * t0 * G::S + pos;
-#pragma unroll
-    for (int t = 0; t < NTI; ++t)
-      if (t < nt) {
+      for (int t = 0; t < NT; ++t) {
         y0[8 * t * G::S] = sgn * c[mt][t][0];
         y1[8 * t * G::S] = sgn * c[mt][t][1];
       }
+    }
+    __syncwarp();
+  }
+}
+
+template <int P, int MT, int KS>
+__device__ __forceinline__ void rot_item(const double* __restrict__ A, const int32_t* pos, int nparts, double sgn1,
+                                         int ntiles, double* xc, int lane, int dbg) {
+  static_assert(RGeo<P>::NT <= 5, "n-tile dispatch covers up to 5");
+  switch (ntiles) {
+    case 1: rot_item_nt<P, MT, KS, 1>(A, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 2: rot_item_nt<P, MT, KS, 2>(A, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 3: rot_item_nt<P, MT, KS, 3>(A, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 4: rot_item_nt<P, MT, KS, 4>(A, pos, nparts, sgn1, xc, lane, dbg); break;
+    default: rot_item_nt<P, MT, KS, RGeo<P>::NT>(A, pos, nparts, sgn1, xc, lane, dbg); break;
   }
 }
 
 // Named barriers: 1/2 Xfull(b) prep -> MMA; 3/4 Yfull(b) MMA -> acc; 7/8 Xfree(b) acc -> prep;
-// 5 MMA warps (between stages); 6 prep warps; 9 acc warps.
+// 5 MMA warps (between stages); 6 prep warps.
 template <int P>
 __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>::NACC), 1)
     m2l_rot_kernel(const RotArgs r, int dbg) {
   using G = RGeo<P>;
-  constexpr int NR = G::NR, NC = G::NC, S = G::S, NCOEF = G::NCOEF, BLOB = rot_blob_size(P);
+  constexpr int NR = G::NR, NC = G::NC, S = G::S, NCOEF = G::NCOEF;
   constexpr int nmma_t = 32 * G::NMMA, nprep_t = 32 * G::NPREP, nacc_t = 32 * G::NACC;
+  const int BLOB = r.blob;
   extern __shared__ double sm[];
   const RotSmem m = rot_carve<P>(sm, r);
   const M2LArgs& a = r.a;
@@ -424,16 +413,14 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
   const int tile = blockIdx.x;
   // ---- shared tables
   for (int e = tid; e < a.T * NR; e += nthr) m.acc[e] = 0.0;
-  for (int q = tid; q < NCOEF; q += nthr) {
-    int n = 0;
-    while (cidx(n + 1, 0) <= q) ++n;
-    m.pairtab[q] = n | ((q - cidx(n, 0)) << 16);
+  for (int k = tid; k < NCOEF - (P + 1); k += nthr) {  // k-th (n, m >= 1) pair
+    int n = 1, kk = k;
+    while (kk >= n) kk -= n, ++n;
+    m.pairtab[k] = n | ((kk + 1) << 16);
   }
   for (int e = tid; e < 3 * G::NMMA * r.smax; e += nthr) m.sched[e] = r.sched[e];
-  for (int e = tid; e < 6 * (P + 1); e += nthr) {
-    const int st = e / (2 * (P + 1)), blk = (e / 2) % (P + 1), pt = e & 1;
-    m.blkoff[e] = pt < rot_block_parts(st, blk) ? rot_block_offset(P, st, blk, pt) : 0;
-  }
+  for (int e = tid; e < r.nitems; e += nthr) m.ihdr[e] = r.ihdr[e];
+  for (int e = tid; e < 32 * r.nitems; e += nthr) m.ipos[e] = r.ipos[e];
   for (int q = tid; q < NR; q += nthr) {
     int n, mm, part;
     ri_decode(P, q, n, mm, part);
@@ -442,8 +429,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
     m.lmask[q] = r.masks[NR + q];
   }
   if (tid == 0) {
-    mbar_init(m.bar, 1);
-    mbar_init(m.bar + 1, 1);
+    for (int j = 0; j < 5; ++j) mbar_init(m.bar + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int c_first = a.tile_chunk[tile], c_last = a.tile_chunk[tile + 1];
@@ -455,28 +441,40 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       const int i = ch - c_first, b = i & 1;
       named_sync(3 + b, nmma_t + nacc_t);  // Yfull(i)
       if (!(dbg & 4)) {
-        const double* y = b ? m.x1 : m.x0;
-        const double* ob = m.ob + b * BLOB;
-        const int ns = m.ncs[2 * b + 1];
-        const int* meta = m.meta + b * NC;
-        const int* sb = m.sbeg + b * (NC + 1);
-        const int* ss = m.sslot + b * NC;
-        for (int row = h; row < NR; row += nacc_t) {
+        const double* __restrict__ y = b ? m.x1 : m.x0;
+        const double* __restrict__ ob = m.ob + b * BLOB;
+        const int32_t* __restrict__ dsc = m.desc + (i % 3) * rot_desc_ints(NC);
+        const int ns = dsc[1];
+        const int* __restrict__ meta = dsc + 4 + NC;
+        const int* __restrict__ ss = dsc + 4 + 2 * NC;
+        const int* __restrict__ sb = dsc + 4 + 3 * NC;
+        double* __restrict__ acc = m.acc;
+        const int2* __restrict__ colt = m.colt + b * NC;
+        constexpr int RG = nacc_t / NR > 0 ? nacc_t / NR : 1;  // threads per row (segment ranges)
+        for (int t = h; t < RG * NR; t += nacc_t) {
+          const int rg = t / NR, row = t - rg * NR;
+          const int s_lo = ns * rg / RG, s_hi = ns * (rg + 1) / RG;
           const int d = m.dec[row], part = d & 1, n = (d >> 1) & 0x7f;
           const int mm = (d >> 8) - cidx(n, 0);
           const int rre = d >> 8, rim = mm ? NCOEF + rre - n - 1 : rre;
           const double ca = mm ? ob[2 * mm] : 1.0, sa = mm ? ob[2 * mm + 1] : 0.0;
+          // column value = c0 yr + c1 yi: source part = part ^ (take partner), then Az_L,
+          // then the sign; idx = mask bits ^ part = (source part) | (negate) << 1
           const uint32_t mask = m.lmask[row];
-          for (int sgi = 0; sgi < ns; ++sgi) {
-            double* ap = m.acc + ss[sgi] * NR + row;
+          // column value = k0 yr + k1 yi: source part = part ^ (take partner), then Az_L,
+          // then the sign (idx = mask bits ^ part = source part | negate << 1)
+          const double kr0 = ca, ki0 = -sa, kr1 = sa, ki1 = ca;
+          for (int sgi = s_lo; sgi < s_hi; ++sgi) {
+            const int ce = sb[sgi + 1];
+            double* ap = acc + ss[sgi] * NR + row;
             double v = *ap;
-            for (int col = sb[sgi]; col < sb[sgi + 1]; ++col) {
-              const uint32_t mg = mask >> (2 * (meta[col] >> 8));
-              const double* yc = y + col_base(col, S);
-              const double yr = yc[rre], yi = yc[rim];
-              const int src = part ^ (int)(mg & 1);  // component of Az_L Y feeding this row
-              const double t0 = src == 0 ? fma(-sa, yi, ca * yr) : fma(ca, yi, sa * yr);
-              v += (mg & 2) ? -t0 : t0;
+            for (int col = sb[sgi]; col < ce; ++col) {
+              const int2 cg = colt[col];  // (column base, 2 g)
+              const int idx = (int)((mask >> cg.y) & 3) ^ part;
+              const double yr = y[cg.x + rre], yi = y[cg.x + rim];
+              double k0 = (idx & 1) ? kr1 : kr0, k1 = (idx & 1) ? ki1 : ki0;
+              const double t = fma(k0, yr, k1 * yi);
+              v = (idx & 2) ? v - t : v + t;
             }
             *ap = v;
           }
@@ -485,21 +483,24 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       named_arrive(7 + b, nacc_t + nprep_t);  // Xfree(i): buffer b may take chunk i + 2
     }
   } else if (warp >= G::NMMA) {
-    // ================= prep warps: metadata, TMA bulk copies, symmetry map + Az_M in place
+    // ================= prep warps: descriptors, TMA bulk copies, symmetry map + Az_M in place
     const int h = tid - nmma_t;
+    constexpr int DI = rot_desc_ints(NC);
+    auto issue_desc = [&](int ch, int j) {  // descriptor of chunk ch into buffer j (one lane)
+      fence_proxy_async();
+      mbar_arrive_tx(m.bar + 2 + j, DI * sizeof(int32_t));
+      bulk_g2s(m.desc + j * DI, r.desc + (int64_t)ch * DI, DI * sizeof(int32_t), m.bar + 2 + j);
+    };
+    if (h == 0 && c_first < c_last) issue_desc(c_first, 0);
     for (int ch = c_first; ch < c_last; ++ch) {
-      const int i = ch - c_first, b = i & 1;
-      if (i >= 2) named_sync(7 + b, nacc_t + nprep_t);  // Xfree(i - 2)
+      const int i = ch - c_first, b = i & 1, j = i % 3;
+      if (i >= 2) named_sync(7 + b, nacc_t + nprep_t);  // Xfree(i - 2): X buffer b, descriptor (i + 1) % 3
+      if (h == 0 && ch + 1 < c_last) issue_desc(ch + 1, (i + 1) % 3);
       double* xb = b ? m.x1 : m.x0;
       double* ob = m.ob + b * BLOB;
-      load_meta_dev(a, ch, m.meta + b * NC, m.srcs + b * NC, m.sslot + b * NC, m.sbeg + b * (NC + 1), h, nprep_t);
-      const int cls = a.chunk_class[ch];
-      const int ncol = a.chunk_begin[ch + 1] - a.chunk_begin[ch];
-      if (h == 0) {
-        m.ncs[2 * b] = ncol;
-        m.ncs[2 * b + 1] = a.chunk_seg[ch + 1] - a.chunk_seg[ch];
-      }
-      named_sync(6, nprep_t);  // metadata visible to the prep warps
+      const int32_t* dsc = m.desc + j * DI;
+      mbar_wait(m.bar + 2 + j, (unsigned)((i / 3) & 1));
+      const int ncol = dsc[0], cls = dsc[2];
       if (h < 32 && !(dbg & 8)) {
         fence_proxy_async();  // earlier generic accesses of xb / ob before the async-proxy writes
         if (h == 0) {
@@ -508,33 +509,60 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
         }
         __syncwarp();
         for (int c = h; c < ncol; c += 32)
-          bulk_g2s(xb + col_base(c, S), a.Mt + (int64_t)m.srcs[b * NC + c] * G::KPAD, G::KPAD * sizeof(double),
-                   m.bar + b);
+          bulk_g2s(xb + col_base(c, S), a.Mt + (int64_t)dsc[4 + c] * G::KPAD, G::KPAD * sizeof(double), m.bar + b);
       }
+      for (int c = h; c < ncol; c += nprep_t) m.colt[b * NC + c] = make_int2(col_base(c, S), 2 * (dsc[4 + NC + c] >> 8));
       const int ncol8 = (ncol + 7) & ~7;  // padding columns of the last n-tile: zeros
       for (int e = h; e < (ncol8 - ncol) * G::KPAD; e += nprep_t)
         xb[col_base(ncol + e / G::KPAD, S) + e % G::KPAD] = 0.0;
       if (!(dbg & 8)) mbar_wait(m.bar + b, (unsigned)((i >> 1) & 1));
       if (!(dbg & 2)) {
-#pragma unroll 4
-        for (int it = h; it < ncol * NCOEF; it += nprep_t) {
-          const int col = it / NCOEF, q = it - col * NCOEF;
-          const int pe = m.pairtab[q], n = pe & 0xffff, mm = pe >> 16;
-          const int g2 = 2 * (m.meta[b * NC + col] >> 8);
-          double* xcol = xb + col_base(col, S);
-          if (mm == 0) {
-            if ((m.mmask[q] >> g2) & 2) xcol[q] = -xcol[q];
-          } else {
-            const int rre = q, rim = NCOEF + q - n - 1;
-            const uint32_t f0 = m.mmask[rre] >> g2, f1 = m.mmask[rim] >> g2;
-            const double v0 = xcol[rre], v1 = xcol[rim];
-            double u0 = (f0 & 1) ? v1 : v0, u1 = (f1 & 1) ? v0 : v1;
-            u0 = (f0 & 2) ? -u0 : u0;
-            u1 = (f1 & 2) ? -u1 : u1;
-            const double cs = ob[2 * mm], sn = ob[2 * mm + 1];
-            xcol[rre] = cs * u0 - sn * u1;
-            xcol[rim] = sn * u0 + cs * u1;
+        // X[col] <- Az_M (D^M_g)^-1 X[col]; item = (column, (n, m >= 1) pair), batches of
+        // four items: all loads, then the arithmetic, then the stores (no smem aliasing stalls)
+        constexpr int NP = NCOEF - (P + 1);  // pairs with m >= 1
+        constexpr int kPB = 6;               // items per batch
+        const int nit = ncol * NP;
+        for (int it0 = h; it0 < nit; it0 += kPB * nprep_t) {
+          double v0[kPB], v1[kPB], cs[kPB], sn[kPB];
+          uint32_t f0[kPB], f1[kPB];
+          int base[kPB], rre[kPB], rim[kPB];
+#pragma unroll
+          for (int u = 0; u < kPB; ++u) {
+            const int it = it0 + u * nprep_t;
+            const int itc = it < nit ? it : 0;
+            const int col = itc / NP, k = itc - col * NP;
+            const int pe = m.pairtab[k], n = pe & 0xffff, mm = pe >> 16;
+            const int g2 = 2 * (dsc[4 + NC + col] >> 8);
+            base[u] = it < nit ? col_base(col, S) : -1;
+            rre[u] = cidx(n, mm);
+            rim[u] = NCOEF + rre[u] - n - 1;
+            f0[u] = m.mmask[rre[u]] >> g2;
+            f1[u] = m.mmask[rim[u]] >> g2;
+            v0[u] = xb[col_base(col, S) + rre[u]];
+            v1[u] = xb[col_base(col, S) + rim[u]];
+            cs[u] = ob[2 * mm];
+            sn[u] = ob[2 * mm + 1];
           }
+#pragma unroll
+          for (int u = 0; u < kPB; ++u) {
+            double u0 = (f0[u] & 1) ? v1[u] : v0[u], u1 = (f1[u] & 1) ? v0[u] : v1[u];
+            u0 = (f0[u] & 2) ? -u0 : u0;
+            u1 = (f1[u] & 2) ? -u1 : u1;
+            v0[u] = cs[u] * u0 - sn[u] * u1;
+            v1[u] = sn[u] * u0 + cs[u] * u1;
+          }
+#pragma unroll
+          for (int u = 0; u < kPB; ++u)
+            if (base[u] >= 0) {
+              xb[base[u] + rre[u]] = v0[u];
+              xb[base[u] + rim[u]] = v1[u];
+            }
+        }
+        // m = 0 entries: sign only
+        for (int it = h; it < ncol * (P + 1); it += nprep_t) {
+          const int col = it / (P + 1), n = it - col * (P + 1), q = cidx(n, 0);
+          const int g2 = 2 * (dsc[4 + NC + col] >> 8);
+          if ((m.mmask[q] >> g2) & 2) xb[col_base(col, S) + q] = -xb[col_base(col, S) + q];
         }
       }
       named_arrive(1 + b, nprep_t + nmma_t);  // Xfull(i)
@@ -546,16 +574,23 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       named_sync(1 + b, nprep_t + nmma_t);  // Xfull(i)
       double* xc = b ? m.x1 : m.x0;
       const double* ob = m.ob + b * BLOB;
-      const int ntiles = (m.ncs[2 * b] + 7) >> 3;
+      const int ntiles = (m.desc[(i % 3) * rot_desc_ints(NC)] + 7) >> 3;
       for (int st = 0; st < 3; ++st) {
         const int32_t* sl = m.sched + (st * G::NMMA + warp) * r.smax;
         for (int k = 0; k < r.smax && !(dbg & 1); ++k) {
-          const int item = sl[k];
-          if (item < 0) break;
-          const int t0 = (item >> 6) & 7, t1 = min(ntiles, t0 + ((item >> 9) & 7));
-          if (t0 < t1) rot_item<P>(ob, m.blkoff, st, item & 0x1f, (item >> 5) & 1, t0, t1, xc, lane);
+          const int id = sl[k];
+          if (id < 0) break;
+          const int hd = m.ihdr[id];
+          const double* A = ob + (hd >> 8);
+          const int32_t* ps = m.ipos + 32 * id;
+          const int nparts = (hd >> 1) & 3;
+          const double sgn1 = st == 1 ? -1.0 : 1.0;  // z translation: Im = -Z Im
+          if (hd & 1)
+            rot_item<P, 2, G::KSB>(A, ps, nparts, sgn1, ntiles, xc, lane, dbg);
+          else
+            rot_item<P, 1, 2>(A, ps, nparts, sgn1, ntiles, xc, lane, dbg);
         }
-        if (st < 2) named_sync(5, nmma_t);  // stage st complete before st + 1 reads it
+        if (st < 2 && !(dbg & 16)) named_sync(5, nmma_t);  // stage st complete before st + 1 reads it
       }
       named_arrive(3 + b, nmma_t + nacc_t);  // Yfull(i)
     }
@@ -629,15 +664,114 @@ void gauss_legendre(int k, std::vector<double>& x, std::vector<double>& w) {
   }
 }
 
+
+// Per-chunk descriptor (one contiguous 16-byte-aligned record, loaded by one TMA bulk copy):
+// [ncol, nseg, class, 0 | srcs[NC] | meta[NC] | sslot[NC] | sbeg[NC + 1]] (sbeg relative to the chunk)
+__global__ void chunk_desc_kernel(const int32_t* __restrict__ chunk_begin, const int32_t* __restrict__ chunk_class,
+                                  const int32_t* __restrict__ chunk_seg, const int32_t* __restrict__ seg_begin,
+                                  const int32_t* __restrict__ col_src, const int32_t* __restrict__ col_meta,
+                                  int64_t nchunks, int NC, int32_t* __restrict__ desc) {
+  const int64_t ch = blockIdx.x;
+  if (ch >= nchunks) return;
+  int32_t* d = desc + ch * rot_desc_ints(NC);
+  const int cb = chunk_begin[ch], ncol = chunk_begin[ch + 1] - cb;
+  const int s0 = chunk_seg[ch], ns = chunk_seg[ch + 1] - s0;
+  for (int t = threadIdx.x; t < rot_desc_ints(NC); t += blockDim.x) {
+    int v = 0;
+    if (t == 0) v = ncol;
+    else if (t == 1) v = ns;
+    else if (t == 2) v = chunk_class[ch];
+    else if (t >= 4 && t < 4 + NC) v = t - 4 < ncol ? col_src[cb + t - 4] : 0;
+    else if (t >= 4 + NC && t < 4 + 2 * NC) v = t - 4 - NC < ncol ? col_meta[cb + t - 4 - NC] : 0;
+    else if (t >= 4 + 2 * NC && t < 4 + 3 * NC) v = t - 4 - 2 * NC < ns ? (col_meta[seg_begin[s0 + t - 4 - 2 * NC]] & 0xff) : 0;
+    else if (t >= 4 + 3 * NC && t <= 4 + 4 * NC) v = t - 4 - 3 * NC <= ns ? seg_begin[s0 + t - 4 - 3 * NC] - cb : 0;
+    d[t] = v;
+  }
+}
+
+// Pack the blocks of every stage into items (first-fit decreasing for the small ones).
+std::vector<RotItem> build_items(int p, int& blob_frag) {
+  std::vector<RotItem> items;
+  int aoff = 2 * (p + 1);
+  for (int st = 0; st < 3; ++st) {
+    struct Blk {
+      int size, code, n0, m0, kind;  // kind 0: D (n, part), 1: Z (m)
+    };
+    std::vector<Blk> blks;
+    if (st == 1) {
+      for (int m = 0; m <= p; ++m) blks.push_back({p + 1 - m, m, 0, m, 1});
+    } else {
+      for (int n = 0; n <= p; ++n) {
+        blks.push_back({n + 1, n, n, 0, 0});
+        if (n > 0) blks.push_back({n, n | (1 << 5), n, 1, 0});
+      }
+    }
+    std::stable_sort(blks.begin(), blks.end(), [](const Blk& x, const Blk& y) { return x.size > y.size; });
+    std::vector<RotItem> bins;
+    std::vector<int> fill;
+    for (const Blk& bk : blks) {
+      int target = -1;
+      if (bk.size <= 8)
+        for (size_t i = 0; i < bins.size(); ++i)
+          if (!bins[i].big && fill[i] + bk.size <= 8) {
+            target = (int)i;
+            break;
+          }
+      if (target < 0) {
+        RotItem it{};
+        it.st = st;
+        it.big = bk.size > 8;
+        it.nparts = st == 1 ? 2 : 1;
+        for (int s = 0; s < 16; ++s) it.slot[s] = -1, it.pos[0][s] = it.pos[1][s] = -1;
+        bins.push_back(it);
+        fill.push_back(0);
+        target = (int)bins.size() - 1;
+      }
+      RotItem& it = bins[target];
+      for (int l = 0; l < bk.size; ++l) {
+        const int s = fill[target] + l;
+        it.slot[s] = bk.code | (l << 8);
+        if (st == 1) {  // order m, degree n = m + l
+          it.pos[0][s] = ri_pos(p, bk.m0 + l, bk.m0, 0);
+          it.pos[1][s] = bk.m0 > 0 ? ri_pos(p, bk.m0 + l, bk.m0, 1) : -1;
+        } else {  // degree n, order m = l (+1 for Im)
+          const int part = (bk.code >> 5) & 1;
+          it.pos[0][s] = ri_pos(p, bk.n0, l + part, part);
+        }
+      }
+      fill[target] += bk.size;
+    }
+    for (RotItem& it : bins) {
+      it.aoff = aoff;
+      aoff += (it.big ? 2 * rot_ksb(p) : 2) * 32;
+      items.push_back(it);
+    }
+  }
+  blob_frag = (aoff + 1) & ~1;
+  return items;
+}
+
 }  // namespace
 
 bool m2l_rot_supported(int p) { return p >= 5 && p <= 14; }
+int rot_chunk_width(int p) { return rot_nc(p); }
+size_t rot_smem_bytes(int p, int T, int extra_ints) {
+  const int NR = (p + 1) * (p + 1), KPAD = (NR + 3) & ~3, S = rot_xstride(KPAD), nc = ncoef(p), NC = rot_nc(p);
+  int blob = 0;
+  std::vector<RotItem> items = build_items(p, blob);
+  const int ni = (int)items.size();
+  return sizeof(double) * ((size_t)T * NR + 2 * (size_t)NC * S + 2 * (size_t)blob) + sizeof(uint64_t) * 6 +
+         sizeof(int32_t) * (3 * rot_desc_ints(NC) + 3 * NR + nc + 2 + 4 * NC + ni + 32 * ni + 3 * 8 * extra_ints);
+}
 
 void m2l_rot_setup(fmm_plan_s& P) {
   M2LDmma& D = P.m2l_dmma;
   cudaStream_t s = P.stream;
   const int p = P.p;
   if (D.nclass == 0 || D.ntiles == 0) return;
+  int blob = 0;
+  std::vector<RotItem> items = build_items(p, blob);
+  const int ni = (int)items.size();
   // quadrature (exact to degree 2p on the sphere)
   std::vector<double> gx, gw;
   gauss_legendre(p + 1, gx, gw);
@@ -651,13 +785,14 @@ void m2l_rot_setup(fmm_plan_s& P) {
   Rs.alloc((int64_t)np * ncoef(p));
   quad_points_kernel<<<cdiv(np * (p + 1), 128), 128, 0, s>>>(dgx, p, Rs);
   FMM_LAUNCHED("quad_points_kernel");
-  D.rot_ops.alloc(D.nclass * rot_blob_size(p));
-  {  // symmetry masks from the signed-permutation tables (m2l_dmma.cu)
+  D.rot_blob = blob;
+  D.rot_ops.alloc(D.nclass * blob);
+  {  // symmetry masks from the signed-permutation tables (m2l_dmma.cu), rows in RI order
     const int NR = (p + 1) * (p + 1);
     std::vector<int32_t> sym = build_symtab(p);
     std::vector<uint32_t> mk(2 * NR, 0);
     for (int which = 0; which < 2; ++which)
-      for (int q = 0; q < NR; ++q) {  // RI row q <-> real index rr
+      for (int q = 0; q < NR; ++q) {
         int n, mm, part;
         ri_decode(p, q, n, mm, part);
         const int rr = real_index(n, mm, part);
@@ -670,6 +805,29 @@ void m2l_rot_setup(fmm_plan_s& P) {
     D.rot_masks.alloc(2 * NR);
     FMM_CUDA(cudaMemcpyAsync(D.rot_masks.ptr, mk.data(), sizeof(uint32_t) * mk.size(), cudaMemcpyHostToDevice, s));
   }
+  // item tables: device copy for the build kernel, headers and positions for the mat-vec
+  std::vector<ItemDev> idev(ni);
+  std::vector<int32_t> hdr(ni), pos(32 * ni);
+  for (int i = 0; i < ni; ++i) {
+    idev[i].st = items[i].st;
+    idev[i].big = items[i].big;
+    idev[i].nparts = items[i].nparts;
+    idev[i].aoff = items[i].aoff;
+    for (int k = 0; k < 16; ++k) idev[i].slot[k] = items[i].slot[k];
+    hdr[i] = items[i].big | (items[i].nparts << 1) | (items[i].aoff << 8);
+    for (int k = 0; k < 16; ++k) {
+      pos[32 * i + k] = items[i].pos[0][k];
+      pos[32 * i + 16 + k] = items[i].pos[1][k];
+    }
+  }
+  DevBuf<ItemDev> ditems;
+  ditems.alloc(ni);
+  FMM_CUDA(cudaMemcpyAsync(ditems.ptr, idev.data(), sizeof(ItemDev) * ni, cudaMemcpyHostToDevice, s));
+  D.rot_ihdr.alloc(ni);
+  D.rot_ipos.alloc(32 * ni);
+  FMM_CUDA(cudaMemcpyAsync(D.rot_ihdr.ptr, hdr.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice, s));
+  FMM_CUDA(cudaMemcpyAsync(D.rot_ipos.ptr, pos.data(), sizeof(int32_t) * 32 * ni, cudaMemcpyHostToDevice, s));
+  D.rot_nitems = ni;
   int nent = 0;
   for (int n = 0; n <= p; ++n) nent += (n + 1) * (n + 1) + n * n;
   const size_t sh = sizeof(double2) * kQuadBatch * ncoef(p) + sizeof(double) * nent;
@@ -678,24 +836,20 @@ void m2l_rot_setup(fmm_plan_s& P) {
     FMM_CUDA(cudaFuncSetAttribute(build_rot_ops_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     configured = sh;
   }
-  build_rot_ops_kernel<<<(unsigned)D.nclass, kRotBuildThreads, sh, s>>>(D.class_keys, p, dgx, dgw, Rs, D.rot_ops);
+  build_rot_ops_kernel<<<(unsigned)D.nclass, kRotBuildThreads, sh, s>>>(D.class_keys, p, dgx, dgw, Rs, ditems, ni,
+                                                                         blob, D.rot_ops);
   FMM_LAUNCHED("build_rot_ops_kernel");
-  // static LPT schedule of the items of each stage over the MMA warps (full 64-column chunk costs)
-  const int nmma = 16;
+  // static LPT schedule of each stage's items over the MMA warps
+  const int nmma = 8;
   std::vector<std::vector<int>> lists(3 * nmma);
   for (int st = 0; st < 3; ++st) {
-    std::vector<std::pair<int, int>> items;  // (cost, code)
-    for (int blk = 0; blk <= p; ++blk) {
-      const int R = rot_block_rows(p, st, blk), mk = ((R + 7) / 8) * ((R + 3) / 4);
-      const int nparts = st == 1 ? (blk > 0 ? 2 : 1) : rot_block_parts(st, blk);
-      const int ntc = rot_chunk_width(p) / 8;  // n-tiles of a full chunk
-      const int nti = std::min(ntc, mk >= 4 ? 2 : 4);  // n-tiles per item: big blocks split finer
-      for (int pt = 0; pt < nparts; ++pt)
-        for (int t0 = 0; t0 < ntc; t0 += nti) items.push_back({mk * nti + 6, blk | (pt << 5) | (t0 << 6) | (nti << 9)});
-    }
-    std::stable_sort(items.begin(), items.end(), [](auto& x, auto& y) { return x.first > y.first; });
+    std::vector<std::pair<int, int>> its;  // (cost, id)
+    for (int i = 0; i < ni; ++i)
+      if (items[i].st == st)
+        its.push_back({(items[i].big ? 2 * rot_ksb(p) : 2) * items[i].nparts * 8 + 24 * items[i].nparts, i});
+    std::stable_sort(its.begin(), its.end(), [](auto& x, auto& y) { return x.first > y.first; });
     std::vector<int> load(nmma, 0);
-    for (auto& it : items) {
+    for (auto& it : its) {
       const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
       load[w] += it.first;
       lists[st * nmma + w].push_back(it.second);
@@ -710,6 +864,10 @@ void m2l_rot_setup(fmm_plan_s& P) {
   D.rot_sched.alloc((int64_t)sched.size());
   FMM_CUDA(cudaMemcpyAsync(D.rot_sched.ptr, sched.data(), sizeof(int32_t) * sched.size(), cudaMemcpyHostToDevice, s));
   D.rot_T = D.T;
+  D.rot_desc.alloc(D.nchunks * rot_desc_ints(D.NC));
+  chunk_desc_kernel<<<(unsigned)D.nchunks, 128, 0, s>>>(D.chunk_begin, D.chunk_class, D.chunk_seg, D.seg_begin,
+                                                         D.col_src, D.col_meta, D.nchunks, D.NC, D.rot_desc);
+  FMM_LAUNCHED("chunk_desc_kernel");
   FMM_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -728,7 +886,12 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
   r.blobs = D.rot_ops;
   r.masks = D.rot_masks;
   r.sched = D.rot_sched;
+  r.ihdr = D.rot_ihdr;
+  r.ipos = D.rot_ipos;
   r.smax = D.rot_smax;
+  r.nitems = D.rot_nitems;
+  r.blob = D.rot_blob;
+  r.desc = D.rot_desc;
   const size_t sh = rot_smem_bytes(P.p, a.T, D.rot_smax);
   void (*k)(const RotArgs, int) = nullptr;
   const char* dbgs = getenv("FMM_M2L_DEBUG");  // timing experiments only (skips work: wrong results)
@@ -750,7 +913,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
     FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     configured[P.p] = sh;
   }
-  k<<<(unsigned)D.ntiles, 32 * (16 + 4 + 4), sh, P.stream>>>(r, dbg);
+  k<<<(unsigned)D.ntiles, 32 * (8 + 4 + 8), sh, P.stream>>>(r, dbg);
   FMM_LAUNCHED("m2l_rot_kernel");
 }
 

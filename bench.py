@@ -340,7 +340,8 @@ def main():
     down_ms = statistics.mean(s[3] for s in stage)
     p = cfg.p
     nc = (p + 1) * (p + 2) // 2
-    m2l_flops = 2.0 * (p + 1) ** 4 * st["n_m2l_pairs"]
+    m2l_dense_flops = 2.0 * (p + 1) ** 4 * st["n_m2l_pairs"]  # SURVEY 8(d) dense-operator convention
+    m2l_flops = st["m2l_flops_per_pair"] * st["n_m2l_pairs"]  # useful flops of the formulation in use
     own_frac = (st["own_end"] - st["own_begin"]) / cfg.n
     p2p_inter = (st["n_p2p_interactions"] - cfg.n) * own_frac
     near_flops = (19.0 if cfg.grad else 11.0) * p2p_inter + (3 if cfg.grad else 1) * 8.0 * nc * cfg.n * own_frac
@@ -369,7 +370,10 @@ def main():
                 "measured_fp64_probe": probe,
                 "stages_ms": {"upward": up_ms, "m2l": m2l_ms, "downward": down_ms, "near": near_ms},
                 "algorithmic_tflops": {"m2l": m2l_flops / (m2l_ms * 1e-3) / 1e12,
-                                       "near": near_flops / (near_ms * 1e-3) / 1e12}}
+                                       "near": near_flops / (near_ms * 1e-3) / 1e12},
+                "m2l_formulation": {"variant": st["m2l_variant"], "flops_per_pair": st["m2l_flops_per_pair"],
+                                    "dense_convention_flops_per_pair": 2.0 * (p + 1) ** 4,
+                                    "dense_equivalent_tflops": m2l_dense_flops / (m2l_ms * 1e-3) / 1e12}}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only, bounded sample)
     cpu = None

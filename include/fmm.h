@@ -94,6 +94,11 @@ typedef struct {
   double t_setup_ms[8];  /* FMM_T_SORT .. FMM_T_SETUP_TOTAL */
   double t_matvec_ms[8]; /* FMM_T_UPWARD .. FMM_T_MATVEC_TOTAL (0 unless timing enabled) */
   int64_t bytes_device;  /* device memory owned by the plan */
+  int m2l_variant;       /* M2L formulation in use: 1 matrix-free O(p^4) per pair, 2 dense class
+                            operators on DMMA, 3 rotation-factored class operators on DMMA */
+  int m2l_pad_;
+  double m2l_flops_per_pair; /* useful flops per M2L pair of that formulation (v3: the three
+                                block stages + the two azimuthal rotations; v1/v2: 2(p+1)^4) */
 } fmm_stats_t;
 
 /*

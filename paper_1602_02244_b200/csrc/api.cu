@@ -10,6 +10,8 @@
 
 namespace {
 
+int ncoef_host(int p) { return (p + 1) * (p + 2) / 2; }
+
 thread_local std::string g_last_error;
 
 fmm_status fail(int status, const std::string& msg) {
@@ -317,6 +319,19 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     out->t_matvec_ms[i] = P->t_matvec[i];
   }
   out->bytes_device = P->bytes();
+  out->m2l_variant = P->m2l_variant;
+  {
+    const double p1 = P->p + 1;
+    if (P->m2l_variant == 3) {  // sum_n (n+1)^2 + n^2 per rotation stage, sum_m (p+1-m)^2 (Re) + (Im, m > 0)
+      double rot = 0, z = 0;
+      for (int n = 0; n <= P->p; ++n) rot += (n + 1.0) * (n + 1.0) + (double)n * n;
+      for (int m = 0; m <= P->p; ++m) z += (m ? 2.0 : 1.0) * (p1 - m) * (p1 - m);
+      const double az = 2.0 * 6.0 * (ncoef_host(P->p) - p1);  // two 2x2 rotations per (n, m >= 1) pair
+      out->m2l_flops_per_pair = 2.0 * (2.0 * rot + z) + az;
+    } else {
+      out->m2l_flops_per_pair = 2.0 * p1 * p1 * p1 * p1;
+    }
+  }
   return FMM_OK;
 }
 

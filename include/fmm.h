@@ -185,6 +185,61 @@ typedef enum {
 } fmm_array;
 FMM_API fmm_status fmm_export(fmm_plan plan, int what, void* dst, int64_t capacity, int64_t* count);
 
+/*
+ * Multi-GPU mat-vec with a local-essential-tree exchange (world_size > 1;
+ * north_star "Morton-ordered domain decomposition, with a local-essential-tree
+ * exchange (boundary multipoles plus halo particles) over NCCL/NVLink";
+ * DESIGN.md §5). Every rank calls fmm_setup with the GLOBAL points (same tree
+ * and lists on every rank) and owns the Morton particle range
+ * [rank_begin[r], rank_begin[r+1]) cut at leaf boundaries. The library builds
+ * the exchange lists and packs/unpacks device buffers; the CALLER moves them
+ * with its collectives (torch.distributed over NCCL), in this order:
+ *   fmm_let_pack_q   (q_local [caller slice]      -> q_send)       all-to-all-v (Q)
+ *   fmm_let_upward   (q_recv                      -> shared_send, m_send)
+ *                    all-gather of shared_send (SHARED), all-to-all-v (M)
+ *   fmm_let_finish   (shared_recv, m_recv         -> phi_send [, grad_send])
+ *                    all-to-all-v (PHI)
+ *   fmm_let_unpack   (phi_recv [, grad_recv]      -> phi_local [, grad_local])
+ * Buffer sizes (doubles) from fmm_let_counts, per peer rank, in rank order:
+ *   Q: counts; M: counts x 2 nc (nc = (p+1)(p+2)/2 complex coefficients);
+ *   SHARED: count x 2 nc (send), world x count x 2 nc (receive, rank-major);
+ *   PHI: counts (x 3 for gradients).
+ * All pointers are device buffers on ex->device, stream ordered. The upward
+ * pass runs only on the owned particles; straddling cells' partial multipoles
+ * are summed in rank order, so results are deterministic and equal the
+ * single-GPU mat-vec up to summation order.
+ */
+typedef enum {
+  FMM_LET_Q_SEND = 0, FMM_LET_Q_RECV, FMM_LET_M_SEND, FMM_LET_M_RECV, FMM_LET_PHI_SEND, FMM_LET_PHI_RECV,
+  FMM_LET_SHARED,     /* [1]: number of shared (straddling) cells */
+  FMM_LET_RANK_BEGIN, /* [world + 1]: owner ranges */
+  /* index lists (fmm_let_lists_host only) */
+  FMM_LET_Q_SEND_ROWS, FMM_LET_Q_RECV_POS, FMM_LET_SHARED_CELLS, FMM_LET_M_SEND_CELLS, FMM_LET_M_RECV_CELLS,
+  FMM_LET_PHI_SEND_IDX, FMM_LET_PHI_RECV_ROWS
+} fmm_let_what;
+/* caller_counts_host: [world] rows of the caller slice of every rank (sum = n). */
+FMM_API fmm_status fmm_let_setup(fmm_plan plan, const int64_t* caller_counts_host);
+/* counts_host: [world] (SHARED: [1], RANK_BEGIN: [world + 1]) host int64 */
+FMM_API fmm_status fmm_let_counts(fmm_plan plan, int what, int64_t* counts_host);
+FMM_API fmm_status fmm_let_pack_q(fmm_plan plan, const double* q_local, double* q_send);
+FMM_API fmm_status fmm_let_upward(fmm_plan plan, const double* q_recv, double* shared_send, double* m_send);
+FMM_API fmm_status fmm_let_finish(fmm_plan plan, const double* shared_recv, const double* m_recv, double* phi_send,
+                                  double* grad_send);
+FMM_API fmm_status fmm_let_unpack(fmm_plan plan, const double* phi_recv, const double* grad_recv, double* phi_local,
+                                  double* grad_local);
+/*
+ * fmm_let_lists_host — the exchange lists of rank `me` from HOST copies of a tree
+ * (no device work; the same host code fmm_let_setup runs). what = one of
+ * fmm_let_what; dst NULL queries *count. Arrays as in fmm_export; caller_off
+ * [world + 1] prefix sums of the caller counts; leaves sorted by first particle.
+ */
+FMM_API fmm_status fmm_let_lists_host(int64_t n, int world, int me, const int64_t* caller_off, const uint32_t* perm,
+                                      int64_t ncells, const int32_t* cbeg, const int32_t* cend, int64_t nleaves,
+                                      const int32_t* leaves, int64_t np2p, const int32_t* p2p_tgt,
+                                      const int32_t* p2p_src, int64_t nm2l, const int32_t* m2l_tgt,
+                                      const int32_t* m2l_src, int what, int64_t* dst, int64_t capacity,
+                                      int64_t* count);
+
 /* fmm_destroy — free the plan (NULL is a no-op). */
 FMM_API void fmm_destroy(fmm_plan plan);
 

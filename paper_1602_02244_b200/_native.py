@@ -16,8 +16,13 @@ FMM_OK, FMM_ERR_USAGE, FMM_ERR_NUMERIC, FMM_ERR_CUDA, FMM_ERR_OOM, FMM_ERR_COMM 
 (FMM_X_KEYS, FMM_X_PERM, FMM_X_LEVEL, FMM_X_ANCHOR, FMM_X_BEGIN, FMM_X_END, FMM_X_CHILD, FMM_X_NCHILD,
  FMM_X_PARENT, FMM_X_CENTER, FMM_X_P2P, FMM_X_M2L, FMM_X_M, FMM_X_L, FMM_X_GEOM) = range(15)
 
+(FMM_LET_Q_SEND, FMM_LET_Q_RECV, FMM_LET_M_SEND, FMM_LET_M_RECV, FMM_LET_PHI_SEND, FMM_LET_PHI_RECV, FMM_LET_SHARED,
+ FMM_LET_RANK_BEGIN, FMM_LET_Q_SEND_ROWS, FMM_LET_Q_RECV_POS, FMM_LET_SHARED_CELLS, FMM_LET_M_SEND_CELLS,
+ FMM_LET_M_RECV_CELLS, FMM_LET_PHI_SEND_IDX, FMM_LET_PHI_RECV_ROWS) = range(15)
 EXPORTED = ("fmm_setup", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
-            "fmm_set_timing", "fmm_export", "fmm_destroy", "fmm_last_error", "fmm_version")
+            "fmm_set_timing", "fmm_export", "fmm_destroy", "fmm_last_error", "fmm_version", "fmm_let_setup",
+            "fmm_let_counts", "fmm_let_pack_q", "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack",
+            "fmm_let_lists_host")
 
 
 class FmmExec(C.Structure):
@@ -65,8 +70,17 @@ def lib() -> C.CDLL:
     L.fmm_destroy.restype = None
     L.fmm_last_error.restype = C.c_char_p
     L.fmm_version.restype = C.c_char_p
+    L.fmm_let_setup.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.fmm_let_counts.argtypes = [vp, C.c_int, C.POINTER(C.c_int64)]
+    L.fmm_let_pack_q.argtypes = [vp, dp, dp]
+    L.fmm_let_upward.argtypes = [vp, dp, dp, dp]
+    L.fmm_let_finish.argtypes = [vp, dp, dp, dp, dp]
+    L.fmm_let_unpack.argtypes = [vp, dp, dp, dp, dp]
+    L.fmm_let_lists_host.argtypes = [i64, C.c_int, C.c_int, vp, vp, i64, vp, vp, i64, vp, i64, vp, vp, i64, vp, vp,
+                                     C.c_int, vp, i64, C.POINTER(C.c_int64)]
     for nm in ("fmm_setup", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
-               "fmm_set_timing", "fmm_export"):
+               "fmm_set_timing", "fmm_export", "fmm_let_setup", "fmm_let_counts", "fmm_let_pack_q",
+               "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack", "fmm_let_lists_host"):
         getattr(L, nm).restype = C.c_int
     _lib = L
     return L

@@ -172,6 +172,7 @@ int64_t fmm_plan_s::bytes() const {
   b += p2p.tgt.bytes() + p2p.src.bytes() + p2p.off.bytes() + m2l.tgt.bytes() + m2l.src.bytes() + m2l.off.bytes();
   b += host_stage_q.bytes() + host_stage_phi.bytes() + host_stage_grad.bytes();
   b += m2l_dmma.bytes();
+  b += let_dev.bytes();
   return b;
 }
 
@@ -401,6 +402,158 @@ fmm_status fmm_export(fmm_plan P, int what, void* dst, int64_t capacity, int64_t
     } else if (cnt > 0) {
       FMM_CUDA(cudaMemcpy(dst, src, esz * cnt, cudaMemcpyDeviceToHost));
     }
+  });
+}
+
+fmm_status fmm_let_setup(fmm_plan P, const int64_t* caller_counts) {
+  if (!P || !caller_counts) return fail(FMM_ERR_USAGE, "fmm_let_setup: NULL argument");
+  if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_let_setup: plan is poisoned by an earlier error");
+  return guarded(P, [&] {
+    usage(P->world > 1, "fmm_let_setup: world_size must be > 1");
+    FMM_CUDA(cudaSetDevice(P->device));
+    fmm::let_setup(*P, caller_counts);
+  });
+}
+
+namespace {
+const std::vector<int64_t>* let_vec(const fmm::LetLists& L, int what) {
+  switch (what) {
+    case FMM_LET_Q_SEND: return &L.q_send;
+    case FMM_LET_Q_RECV: return &L.q_recv;
+    case FMM_LET_M_SEND: return &L.m_send;
+    case FMM_LET_M_RECV: return &L.m_recv;
+    case FMM_LET_PHI_SEND: return &L.phi_send;
+    case FMM_LET_PHI_RECV: return &L.phi_recv;
+    case FMM_LET_RANK_BEGIN: return &L.rank_begin;
+    case FMM_LET_Q_SEND_ROWS: return &L.q_send_rows;
+    case FMM_LET_Q_RECV_POS: return &L.q_recv_pos;
+    case FMM_LET_PHI_SEND_IDX: return &L.phi_send_idx;
+    case FMM_LET_PHI_RECV_ROWS: return &L.phi_recv_rows;
+    default: return nullptr;
+  }
+}
+void let_require(fmm_plan_s* P) { usage(P->let_ready, "fmm_let_*: call fmm_let_setup first"); }
+}  // namespace
+
+fmm_status fmm_let_counts(fmm_plan P, int what, int64_t* out) {
+  if (!P || !out) return fail(FMM_ERR_USAGE, "fmm_let_counts: NULL argument");
+  return guarded(P, [&] {
+    let_require(P);
+    if (what == FMM_LET_SHARED) {
+      out[0] = (int64_t)P->let.shared.size();
+      return;
+    }
+    usage(what >= FMM_LET_Q_SEND && what <= FMM_LET_RANK_BEGIN, "fmm_let_counts: unknown what");
+    const std::vector<int64_t>* v = let_vec(P->let, what);
+    std::copy(v->begin(), v->end(), out);
+  });
+}
+
+fmm_status fmm_let_pack_q(fmm_plan P, const double* q_local, double* q_send) {
+  if (!P) return fail(FMM_ERR_USAGE, "fmm_let_pack_q: plan is NULL");
+  if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_let_pack_q: plan is poisoned by an earlier error");
+  return guarded(P, [&] {
+    let_require(P);
+    usage(P->let.q_send_rows.empty() || (q_local && q_send), "fmm_let_pack_q: NULL buffer");
+    FMM_CUDA(cudaSetDevice(P->device));
+    fmm::let_pack_q(*P, q_local, q_send);
+  });
+}
+
+fmm_status fmm_let_upward(fmm_plan P, const double* q_recv, double* shared_send, double* m_send) {
+  if (!P) return fail(FMM_ERR_USAGE, "fmm_let_upward: plan is NULL");
+  if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_let_upward: plan is poisoned by an earlier error");
+  return guarded(P, [&] {
+    let_require(P);
+    usage((P->let.q_recv_pos.empty() || q_recv) && (P->let.shared.empty() || shared_send) &&
+              (P->let.m_send_cells.empty() || m_send),
+          "fmm_let_upward: NULL buffer");
+    FMM_CUDA(cudaSetDevice(P->device));
+    Timer T(*P, P->timing);
+    T.mark(0);
+    fmm::let_upward(*P, q_recv, shared_send, m_send);
+    T.mark(1);
+    if (T.on) {
+      FMM_CUDA(cudaEventSynchronize(P->ev[1]));
+      P->t_matvec[FMM_T_UPWARD] = T.between(0, 1);
+    }
+  });
+}
+
+fmm_status fmm_let_finish(fmm_plan P, const double* shared_recv, const double* m_recv, double* phi_send,
+                          double* grad_send) {
+  if (!P) return fail(FMM_ERR_USAGE, "fmm_let_finish: plan is NULL");
+  if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_let_finish: plan is poisoned by an earlier error");
+  return guarded(P, [&] {
+    let_require(P);
+    usage((P->let.shared.empty() || shared_recv) && (P->let.m_recv_cells.empty() || m_recv) &&
+              (P->let.phi_send_idx.empty() || phi_send),
+          "fmm_let_finish: NULL buffer");
+    FMM_CUDA(cudaSetDevice(P->device));
+    Timer T(*P, P->timing);
+    T.mark(1);
+    fmm::let_exchange_in(*P, shared_recv, m_recv);
+    if (P->m2l_variant >= 2)
+      fmm::m2l_dmma_pass(*P);
+    else
+      fmm::m2l_pass(*P);
+    T.mark(2);
+    fmm::downward(*P);
+    T.mark(3);
+    P->near_compact_out = true;
+    fmm::near_pass_warp(*P, P->let_dev.phi_own.ptr, grad_send ? P->let_dev.grad_own.ptr : nullptr);
+    P->near_compact_out = false;
+    fmm::let_pack_phi(*P, phi_send, grad_send);
+    T.mark(4);
+    if (T.on) {
+      FMM_CUDA(cudaEventSynchronize(P->ev[4]));
+      P->t_matvec[FMM_T_M2L] = T.between(1, 2);
+      P->t_matvec[FMM_T_DOWNWARD] = T.between(2, 3);
+      P->t_matvec[FMM_T_NEAR] = T.between(3, 4);
+    }
+  });
+}
+
+fmm_status fmm_let_unpack(fmm_plan P, const double* phi_recv, const double* grad_recv, double* phi_local,
+                          double* grad_local) {
+  if (!P) return fail(FMM_ERR_USAGE, "fmm_let_unpack: plan is NULL");
+  if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_let_unpack: plan is poisoned by an earlier error");
+  return guarded(P, [&] {
+    let_require(P);
+    usage(P->let.phi_recv_rows.empty() || (phi_recv && phi_local), "fmm_let_unpack: NULL buffer");
+    FMM_CUDA(cudaSetDevice(P->device));
+    fmm::let_unpack(*P, phi_recv, grad_recv, phi_local, grad_local);
+  });
+}
+
+fmm_status fmm_let_lists_host(int64_t n, int world, int me, const int64_t* caller_off, const uint32_t* perm,
+                              int64_t ncells, const int32_t* cbeg, const int32_t* cend, int64_t nleaves,
+                              const int32_t* leaves, int64_t np2p, const int32_t* p2p_tgt, const int32_t* p2p_src,
+                              int64_t nm2l, const int32_t* m2l_tgt, const int32_t* m2l_src, int what, int64_t* dst,
+                              int64_t capacity, int64_t* count) {
+  return guarded(nullptr, [&] {
+    usage(count != nullptr && world >= 1 && me >= 0 && me < world && n >= 1, "fmm_let_lists_host: bad arguments");
+    usage(caller_off && perm && cbeg && cend && leaves, "fmm_let_lists_host: NULL array");
+    fmm::LetLists L;
+    fmm::let_lists(n, world, me, caller_off, perm, ncells, cbeg, cend, nleaves, leaves, np2p, p2p_tgt, p2p_src, nm2l,
+                   m2l_tgt, m2l_src, L);
+    std::vector<int64_t> tmp;
+    const std::vector<int64_t>* v = let_vec(L, what);
+    if (what == FMM_LET_SHARED) {
+      tmp = {(int64_t)L.shared.size()};
+      v = &tmp;
+    } else if (what == FMM_LET_SHARED_CELLS || what == FMM_LET_M_SEND_CELLS || what == FMM_LET_M_RECV_CELLS) {
+      const std::vector<int32_t>& c = what == FMM_LET_SHARED_CELLS ? L.shared
+                                     : what == FMM_LET_M_SEND_CELLS ? L.m_send_cells
+                                                                    : L.m_recv_cells;
+      tmp.assign(c.begin(), c.end());
+      v = &tmp;
+    }
+    usage(v != nullptr, "fmm_let_lists_host: unknown what");
+    *count = (int64_t)v->size();
+    if (!dst) return;
+    usage(capacity >= *count, "fmm_let_lists_host: capacity too small");
+    std::copy(v->begin(), v->end(), dst);
   });
 }
 

@@ -181,14 +181,15 @@ __global__ void l2l_kernel(int64_t lb, const int32_t* __restrict__ child, const 
 
 }  // namespace
 
-void upward(fmm_plan_s& P) {
+namespace {
+void upward_impl(fmm_plan_s& P, int64_t leaf_b, int64_t leaf_e) {
   cudaStream_t s = P.stream;
   const int nc = P.nc;
-  if (P.nleaves > 0) {
+  if (leaf_e > leaf_b) {
     const size_t sh = sizeof(double2) * kP2MChunk * nc;
     if (sh > 48 * 1024) FMM_CUDA(cudaFuncSetAttribute(p2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    p2m_kernel<<<(unsigned)P.nleaves, kExpThreads, sh, s>>>(
-        P.leaves, P.cells.begin, P.cells.end, P.cells.center, P.pos, P.p, nc, P.M);
+    p2m_kernel<<<(unsigned)(leaf_e - leaf_b), kExpThreads, sh, s>>>(
+        P.leaves.ptr + leaf_b, P.cells.begin, P.cells.end, P.cells.center, P.pos, P.p, nc, P.M);
     FMM_LAUNCHED("p2m_kernel");
   }
   const size_t sh = sizeof(double2) * 24 * nc;
@@ -204,6 +205,10 @@ void upward(fmm_plan_s& P) {
     FMM_LAUNCHED("m2m_kernel");
   }
 }
+}  // namespace
+
+void upward(fmm_plan_s& P) { upward_impl(P, 0, P.nleaves); }
+void upward_own(fmm_plan_s& P) { upward_impl(P, P.own_leaf_begin, P.own_leaf_end); }
 
 void m2l_pass(fmm_plan_s& P) {
   const int nc = P.nc;

@@ -1,0 +1,331 @@
+// let.cu — S14 multi-GPU mat-vec with a local-essential-tree (LET) exchange
+// (north_star: "partitioned across the 8xB200 box by Morton-ordered domain
+// decomposition, with a local-essential-tree exchange (boundary multipoles plus
+// halo particles) over NCCL/NVLink").
+//
+// Every rank holds the same global tree and interaction lists (built by fmm_setup
+// from the all-gathered points), so the approximation is the single-GPU one
+// (reading R12). Rank r owns the Morton particle range [B_r, B_{r+1}) cut at leaf
+// boundaries. Per mat-vec (the caller moves the buffers with its collectives):
+//   1. q: each rank sends every charge of its caller slice to the owner of the
+//      particle and to every rank whose near field needs it (halo leaves);
+//   2. upward pass on the owned particles only: P2M of own leaves, M2M of every
+//      cell (cells outside the range stay exactly zero, so a cell straddling
+//      several ranks holds this rank's PARTIAL multipole, by linearity of M2M);
+//   3. shared (straddling) cells: all partials are all-gathered and summed in
+//      rank order (deterministic); boundary multipoles: each rank sends the
+//      complete multipoles of its own cells that are M2L sources of another
+//      rank's targets;
+//   4. M2L for the targets overlapping the range, L2L, near field of own leaves
+//      (halo charges received in step 1), results in owned Morton order;
+//   5. results are routed back to the callers' slices.
+// Index lists are built on the host at fmm_let_setup from the global tree; the
+// moves are gathers/scatters on the device. let_lists() is plain host code with
+// no CUDA calls (tested on CPU against a brute-force model, tests/test_let.py).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "plan.h"
+
+namespace fmm {
+
+// ----------------------------------------------------------------------------- host
+// Owner range cuts: first leaf whose begin >= r * n / world, for r = 0..world.
+std::vector<int64_t> let_cuts(const int32_t* leaf_begin_sorted, int64_t nleaves, int64_t n, int world) {
+  std::vector<int64_t> B(world + 1);
+  for (int r = 0; r <= world; ++r) {
+    const int64_t target = (int64_t)r * n / world;
+    int64_t lo = 0, hi = nleaves;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (leaf_begin_sorted[mid] < target)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    B[r] = lo < nleaves ? leaf_begin_sorted[lo] : n;
+  }
+  B[0] = 0;
+  B[world] = n;
+  return B;
+}
+
+namespace {
+int find_rank(const std::vector<int64_t>& off, int64_t x) {  // off[r] <= x < off[r+1]
+  return (int)(std::upper_bound(off.begin(), off.end(), x) - off.begin()) - 1;
+}
+}  // namespace
+
+// All index lists of rank `me` (host arrays in, host vectors out). See fmm.h fmm_let_*.
+void let_lists(int64_t n, int world, int me, const int64_t* caller_off /*[world+1]*/, const uint32_t* perm,
+               int64_t ncells, const int32_t* cbeg, const int32_t* cend, int64_t nleaves,
+               const int32_t* leaves /*sorted by begin*/, int64_t np2p, const int32_t* p2p_tgt,
+               const int32_t* p2p_src, int64_t nm2l, const int32_t* m2l_tgt, const int32_t* m2l_src,
+               LetLists& out) {
+  std::vector<int32_t> lbeg(nleaves);
+  for (int64_t i = 0; i < nleaves; ++i) lbeg[i] = cbeg[leaves[i]];
+  const std::vector<int64_t> B = let_cuts(lbeg.data(), nleaves, n, world);
+  const std::vector<int64_t> C(caller_off, caller_off + world + 1);
+  out.world = world;
+  out.rank_begin = B;
+  auto owner = [&](int64_t s) { return find_rank(B, s); };
+  auto caller = [&](int64_t s) { return find_rank(C, (int64_t)perm[s]); };
+  // ---- halo leaves of every rank: P2P sources outside the range of the target's owner
+  std::vector<std::vector<int32_t>> halo(world);
+  for (int64_t k = 0; k < np2p; ++k) {
+    const int t = p2p_tgt[k], s = p2p_src[k];
+    const int d = owner(cbeg[t]);
+    if (owner(cbeg[s]) != d) halo[d].push_back(s);
+  }
+  for (auto& h : halo) {
+    std::sort(h.begin(), h.end(), [&](int a, int b) { return cbeg[a] < cbeg[b]; });
+    h.erase(std::unique(h.begin(), h.end()), h.end());
+  }
+  // positions needed by rank d: its range and its halo leaves, ascending
+  auto needed = [&](int d, std::vector<int64_t>& pos) {
+    pos.clear();
+    size_t hi = 0;
+    int64_t s = B[d];
+    // merge the owned range with the halo ranges (all disjoint from it)
+    while (true) {
+      const int64_t hb = hi < halo[d].size() ? cbeg[halo[d][hi]] : INT64_MAX;
+      if (s < B[d + 1] && s < hb) {
+        pos.push_back(s++);
+      } else if (hi < halo[d].size()) {
+        for (int64_t x = cbeg[halo[d][hi]]; x < cend[halo[d][hi]]; ++x) pos.push_back(x);
+        ++hi;
+      } else {
+        break;
+      }
+    }
+  };
+  // ---- q: send (my caller rows -> each d), receive (positions from each r)
+  out.q_send.assign(world, 0);
+  out.q_recv.assign(world, 0);
+  out.q_send_rows.clear();
+  out.q_recv_pos.clear();
+  std::vector<int64_t> pos;
+  for (int d = 0; d < world; ++d) {
+    needed(d, pos);
+    for (int64_t s : pos)
+      if (caller(s) == me) {
+        out.q_send_rows.push_back((int64_t)perm[s] - C[me]);
+        ++out.q_send[d];
+      }
+  }
+  needed(me, pos);
+  for (int r = 0; r < world; ++r)
+    for (int64_t s : pos)
+      if (caller(s) == r) {
+        out.q_recv_pos.push_back(s);
+        ++out.q_recv[r];
+      }
+  // ---- shared cells (straddling at least two ranges), cell order
+  out.shared.clear();
+  std::vector<char> is_shared(ncells, 0);
+  for (int64_t c = 0; c < ncells; ++c)
+    if (cend[c] > cbeg[c] && owner(cbeg[c]) != owner(cend[c] - 1)) {
+      out.shared.push_back((int32_t)c);
+      is_shared[c] = 1;
+    }
+  // ---- boundary multipoles: (cell owner r) -> (rank d whose targets use it), unique, cell order
+  std::vector<std::vector<int32_t>> need_from(world);  // me receives from r
+  std::vector<std::vector<int32_t>> send_to(world);    // me sends to d
+  for (int64_t k = 0; k < nm2l; ++k) {
+    const int t = m2l_tgt[k], s = m2l_src[k];
+    if (is_shared[s]) continue;
+    const int os = owner(cbeg[s]);
+    const int d0 = owner(cbeg[t]), d1 = owner(cend[t] - 1);
+    for (int d = d0; d <= d1; ++d) {
+      if (d == os) continue;
+      if (d == me) need_from[os].push_back(s);
+      if (os == me) send_to[d].push_back(s);
+    }
+  }
+  out.m_send.assign(world, 0);
+  out.m_recv.assign(world, 0);
+  out.m_send_cells.clear();
+  out.m_recv_cells.clear();
+  for (int r = 0; r < world; ++r) {
+    auto& a = send_to[r];
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+    out.m_send[r] = (int64_t)a.size();
+    out.m_send_cells.insert(out.m_send_cells.end(), a.begin(), a.end());
+    auto& b = need_from[r];
+    std::sort(b.begin(), b.end());
+    b.erase(std::unique(b.begin(), b.end()), b.end());
+    out.m_recv[r] = (int64_t)b.size();
+    out.m_recv_cells.insert(out.m_recv_cells.end(), b.begin(), b.end());
+  }
+  // ---- results: my owned positions -> their caller rank; positions whose caller is me, by owner
+  out.phi_send.assign(world, 0);
+  out.phi_recv.assign(world, 0);
+  out.phi_send_idx.clear();
+  out.phi_recv_rows.clear();
+  for (int r = 0; r < world; ++r)
+    for (int64_t s = B[me]; s < B[me + 1]; ++s)
+      if (caller(s) == r) {
+        out.phi_send_idx.push_back(s - B[me]);
+        ++out.phi_send[r];
+      }
+  for (int d = 0; d < world; ++d)
+    for (int64_t s = B[d]; s < B[d + 1]; ++s)
+      if (caller(s) == me) {
+        out.phi_recv_rows.push_back((int64_t)perm[s] - C[me]);
+        ++out.phi_recv[d];
+      }
+}
+
+// ----------------------------------------------------------------------------- device
+namespace {
+
+__global__ void gather_rows_kernel(const double* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                                   int width, double* __restrict__ dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * width) return;
+  const int64_t k = e / width;
+  dst[e] = src[idx[k] * width + (e - k * width)];
+}
+
+__global__ void scatter_rows_kernel(const double* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                                    int width, double* __restrict__ dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * width) return;
+  const int64_t k = e / width;
+  dst[idx[k] * width + (e - k * width)] = src[e];
+}
+
+// received charges into pos[].w of their (Morton) positions; non-finite flagged
+__global__ void scatter_q_kernel(const double* __restrict__ q, const int64_t* __restrict__ pos_idx, int64_t n,
+                                 double4* __restrict__ pos, int32_t* __restrict__ flags) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (k < n) {
+    const double v = q[k];
+    bad = !isfinite(v);
+    pos[pos_idx[k]].w = v;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1);
+}
+
+// M[shared c] = sum over ranks r (in rank order) of the partials recv[r][k]
+__global__ void sum_shared_kernel(const double* __restrict__ recv, const int32_t* __restrict__ cells, int64_t ns,
+                                  int world, int ncd, double* __restrict__ M) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ns * ncd) return;
+  const int64_t k = e / ncd;
+  double v = 0.0;
+  for (int r = 0; r < world; ++r) v += recv[((int64_t)r * ns + k) * ncd + (e - k * ncd)];
+  M[(int64_t)cells[k] * ncd + (e - k * ncd)] = v;
+}
+
+template <typename T>
+void upload(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
+  d.alloc((int64_t)h.size());
+  if (!h.empty()) FMM_CUDA(cudaMemcpyAsync(d.ptr, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, s));
+}
+
+}  // namespace
+
+void let_setup(fmm_plan_s& P, const int64_t* caller_counts) {
+  cudaStream_t s = P.stream;
+  std::vector<int64_t> C(P.world + 1, 0);
+  for (int r = 0; r < P.world; ++r) {
+    if (caller_counts[r] < 0) throw Error(FMM_ERR_USAGE, "fmm_let_setup: negative caller count");
+    C[r + 1] = C[r] + caller_counts[r];
+  }
+  if (C[P.world] != P.n) throw Error(FMM_ERR_USAGE, "fmm_let_setup: caller counts do not sum to n");
+  const int64_t nc = P.cells.n;
+  std::vector<uint32_t> perm(P.n);
+  std::vector<int32_t> cb(nc), ce(nc), lv(P.nleaves), pt(P.p2p.n), ps(P.p2p.n), mt(P.m2l.n), ms(P.m2l.n);
+  auto d2h = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes) FMM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+  };
+  d2h(perm.data(), P.perm.ptr, sizeof(uint32_t) * P.n);
+  d2h(cb.data(), P.cells.begin.ptr, sizeof(int32_t) * nc);
+  d2h(ce.data(), P.cells.end.ptr, sizeof(int32_t) * nc);
+  d2h(lv.data(), P.leaves.ptr, sizeof(int32_t) * P.nleaves);
+  d2h(pt.data(), P.p2p.tgt.ptr, sizeof(int32_t) * P.p2p.n);
+  d2h(ps.data(), P.p2p.src.ptr, sizeof(int32_t) * P.p2p.n);
+  d2h(mt.data(), P.m2l.tgt.ptr, sizeof(int32_t) * P.m2l.n);
+  d2h(ms.data(), P.m2l.src.ptr, sizeof(int32_t) * P.m2l.n);
+  FMM_CUDA(cudaStreamSynchronize(s));
+  LetLists& L = P.let;
+  let_lists(P.n, P.world, P.rank, C.data(), perm.data(), nc, cb.data(), ce.data(), P.nleaves, lv.data(), P.p2p.n,
+            pt.data(), ps.data(), P.m2l.n, mt.data(), ms.data(), L);
+  // this rank's range must be the one choose_own_range picked (same cut rule)
+  if (L.rank_begin[P.rank] != P.own_begin || L.rank_begin[P.rank + 1] != P.own_end)
+    throw Error(FMM_ERR_CUDA, "fmm_let_setup: owner range mismatch");
+  upload(P.let_dev.q_send_rows, L.q_send_rows, s);
+  upload(P.let_dev.q_recv_pos, L.q_recv_pos, s);
+  std::vector<int64_t> sh(L.shared.begin(), L.shared.end()), msend(L.m_send_cells.begin(), L.m_send_cells.end()),
+      mrecv(L.m_recv_cells.begin(), L.m_recv_cells.end());
+  upload(P.let_dev.shared, sh, s);
+  upload(P.let_dev.m_send_cells, msend, s);
+  upload(P.let_dev.m_recv_cells, mrecv, s);
+  upload(P.let_dev.phi_send_idx, L.phi_send_idx, s);
+  upload(P.let_dev.phi_recv_rows, L.phi_recv_rows, s);
+  std::vector<int32_t> sh32(L.shared.begin(), L.shared.end());
+  upload(P.let_dev.shared32, sh32, s);
+  P.let_dev.phi_own.alloc(std::max<int64_t>(1, P.own_end - P.own_begin));
+  P.let_dev.grad_own.alloc(std::max<int64_t>(1, 3 * (P.own_end - P.own_begin)));
+  P.let_ready = true;
+  FMM_CUDA(cudaStreamSynchronize(s));
+}
+
+namespace {
+void gather(const double* src, const DevBuf<int64_t>& idx, int width, double* dst, cudaStream_t s) {
+  const int64_t n = idx.count;
+  if (n == 0) return;
+  gather_rows_kernel<<<cdiv(n * width, 256), 256, 0, s>>>(src, idx.ptr, n, width, dst);
+  FMM_LAUNCHED("gather_rows_kernel");
+}
+void scatter(const double* src, const DevBuf<int64_t>& idx, int width, double* dst, cudaStream_t s) {
+  const int64_t n = idx.count;
+  if (n == 0) return;
+  scatter_rows_kernel<<<cdiv(n * width, 256), 256, 0, s>>>(src, idx.ptr, n, width, dst);
+  FMM_LAUNCHED("scatter_rows_kernel");
+}
+}  // namespace
+
+void let_pack_q(fmm_plan_s& P, const double* q_local, double* send) {
+  gather(q_local, P.let_dev.q_send_rows, 1, send, P.stream);
+}
+
+void let_upward(fmm_plan_s& P, const double* q_recv, double* shared_send, double* m_send) {
+  cudaStream_t s = P.stream;
+  const int64_t n = P.let_dev.q_recv_pos.count;
+  if (n > 0) {
+    scatter_q_kernel<<<cdiv(n, 256), 256, 0, s>>>(q_recv, P.let_dev.q_recv_pos.ptr, n, P.pos, P.flags);
+    FMM_LAUNCHED("scatter_q_kernel");
+  }
+  FMM_CUDA(cudaMemsetAsync(P.M.ptr, 0, sizeof(double2) * P.M.count, s));  // cells outside the range stay 0
+  upward_own(P);
+  gather((const double*)P.M.ptr, P.let_dev.shared, 2 * P.nc, shared_send, s);
+  gather((const double*)P.M.ptr, P.let_dev.m_send_cells, 2 * P.nc, m_send, s);
+}
+
+void let_exchange_in(fmm_plan_s& P, const double* shared_recv, const double* m_recv) {
+  cudaStream_t s = P.stream;
+  const int64_t ns = P.let_dev.shared32.count, ncd = 2 * P.nc;
+  if (ns > 0) {
+    sum_shared_kernel<<<cdiv(ns * ncd, 256), 256, 0, s>>>(shared_recv, P.let_dev.shared32.ptr, ns, P.world, (int)ncd,
+                                                           (double*)P.M.ptr);
+    FMM_LAUNCHED("sum_shared_kernel");
+  }
+  scatter(m_recv, P.let_dev.m_recv_cells, (int)ncd, (double*)P.M.ptr, s);
+}
+
+void let_pack_phi(fmm_plan_s& P, double* phi_send, double* grad_send) {
+  gather(P.let_dev.phi_own.ptr, P.let_dev.phi_send_idx, 1, phi_send, P.stream);
+  if (grad_send) gather(P.let_dev.grad_own.ptr, P.let_dev.phi_send_idx, 3, grad_send, P.stream);
+}
+
+void let_unpack(fmm_plan_s& P, const double* phi_recv, const double* grad_recv, double* phi, double* grad) {
+  scatter(phi_recv, P.let_dev.phi_recv_rows, 1, phi, P.stream);
+  if (grad && grad_recv) scatter(grad_recv, P.let_dev.phi_recv_rows, 3, grad, P.stream);
+}
+
+}  // namespace fmm

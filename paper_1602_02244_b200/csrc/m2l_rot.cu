@@ -77,6 +77,10 @@ constexpr int rot_xstride(int kpad) {
 }
 // chunk width (columns) of the v3 kernel and its shared-memory budget
 constexpr int rot_nc(int p) { return p <= 10 ? 40 : 32; }
+#ifndef FMM_ROT_MMA
+#define FMM_ROT_MMA 12
+#endif
+constexpr int kRotMMA = FMM_ROT_MMA;  // MMA warps of the v3 kernel
 constexpr int rot_ksb(int p) { return (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB)
 // ints of one per-chunk descriptor: [ncol, nseg, class, 0 | srcs | meta | sslot | sbeg[NC + 1]]
 constexpr int rot_desc_ints(int nc) { return (4 + 4 * nc + 1 + 3) & ~3; }
@@ -265,7 +269,7 @@ struct RGeo {
   static constexpr int S = rot_xstride(KPAD);  // column stride (see col_base)
   static constexpr int NC = rot_nc(P);
   static constexpr int NT = NC / 8;
-  static constexpr int NMMA = 8, NPREP = 4, NACC = 8;
+  static constexpr int NMMA = kRotMMA, NPREP = 4, NACC = 8;
   static constexpr int KSB = rot_ksb(P);
   static constexpr int NCOEF = (P + 1) * (P + 2) / 2;
 };
@@ -761,7 +765,7 @@ size_t rot_smem_bytes(int p, int T, int extra_ints) {
   std::vector<RotItem> items = build_items(p, blob);
   const int ni = (int)items.size();
   return sizeof(double) * ((size_t)T * NR + 2 * (size_t)NC * S + 2 * (size_t)blob) + sizeof(uint64_t) * 6 +
-         sizeof(int32_t) * (3 * rot_desc_ints(NC) + 3 * NR + nc + 2 + 4 * NC + ni + 32 * ni + 3 * 8 * extra_ints);
+         sizeof(int32_t) * (3 * rot_desc_ints(NC) + 3 * NR + nc + 2 + 4 * NC + ni + 32 * ni + 3 * kRotMMA * extra_ints);
 }
 
 void m2l_rot_setup(fmm_plan_s& P) {
@@ -840,7 +844,7 @@ void m2l_rot_setup(fmm_plan_s& P) {
                                                                          blob, D.rot_ops);
   FMM_LAUNCHED("build_rot_ops_kernel");
   // static LPT schedule of each stage's items over the MMA warps
-  const int nmma = 8;
+  const int nmma = kRotMMA;
   std::vector<std::vector<int>> lists(3 * nmma);
   for (int st = 0; st < 3; ++st) {
     std::vector<std::pair<int, int>> its;  // (cost, id)
@@ -913,7 +917,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
     FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     configured[P.p] = sh;
   }
-  k<<<(unsigned)D.ntiles, 32 * (8 + 4 + 8), sh, P.stream>>>(r, dbg);
+  k<<<(unsigned)D.ntiles, 32 * (kRotMMA + 4 + 8), sh, P.stream>>>(r, dbg);
   FMM_LAUNCHED("m2l_rot_kernel");
 }
 

@@ -105,6 +105,7 @@ struct NearArgs {
   double* phi_out;
   double* grad_out;
   int max_tpl, max_g;  // layout limits (tuning; defaults max_tpl<kGrad>(), 8)
+  int64_t out_base;    // perm == nullptr: results at (sorted position - out_base) (LET, owned order)
 };
 
 // Targets [t0, t0 + cnt) of `leaf` as (32 / G) groups x TPL targets per lane.
@@ -204,7 +205,7 @@ __device__ void process_group(const NearArgs& a, int leaf, int t0, int cnt, int 
     const int t = tl + ngrp * kk;
     if (kk < TPL && t < cnt) {
       l2p_eval<kGrad>(Lc, a.p, x.x - c.x, x.y - c.y, x.z - c.z, ff, gg);
-      const int64_t o = a.perm[t0 + t];
+      const int64_t o = a.perm ? (int64_t)a.perm[t0 + t] : (int64_t)(t0 + t) - a.out_base;
       a.phi_out[o] = ff * a.s_phi;
       if (kGrad) {
         a.grad_out[3 * o] = gg.x * a.s_grad;
@@ -277,7 +278,8 @@ void near_pass_warp(fmm_plan_s& P, double* phi, double* grad) {
   a.L = P.L;
   a.off = P.p2p.off;
   a.src = P.p2p.src;
-  a.perm = P.perm;
+  a.perm = P.near_compact_out ? nullptr : P.perm.ptr;
+  a.out_base = P.own_begin;
   a.p = P.p;
   a.nc = P.nc;
   a.s_phi = std::ldexp(1.0, -P.e);

@@ -102,6 +102,28 @@ struct M2LDmma {
   }
 };
 
+// LET exchange lists of one rank (let.cu); counts per peer rank, index lists concatenated in rank order.
+struct LetLists {
+  int world = 1;
+  std::vector<int64_t> rank_begin;                   // [world + 1] owner ranges (Morton positions)
+  std::vector<int64_t> q_send, q_recv;               // charges: my caller rows -> d, positions from r
+  std::vector<int64_t> q_send_rows, q_recv_pos;
+  std::vector<int32_t> shared;                       // straddling cells (all-gathered partials)
+  std::vector<int64_t> m_send, m_recv;               // boundary multipoles (cells)
+  std::vector<int32_t> m_send_cells, m_recv_cells;
+  std::vector<int64_t> phi_send, phi_recv;           // results: owned index -> caller rows
+  std::vector<int64_t> phi_send_idx, phi_recv_rows;
+};
+struct LetDev {
+  DevBuf<int64_t> q_send_rows, q_recv_pos, shared, m_send_cells, m_recv_cells, phi_send_idx, phi_recv_rows;
+  DevBuf<int32_t> shared32;
+  DevBuf<double> phi_own, grad_own;  // owned results in Morton order
+  int64_t bytes() const {
+    return q_send_rows.bytes() + q_recv_pos.bytes() + shared.bytes() + m_send_cells.bytes() + m_recv_cells.bytes() +
+           phi_send_idx.bytes() + phi_recv_rows.bytes() + shared32.bytes() + phi_own.bytes() + grad_own.bytes();
+  }
+};
+
 }  // namespace fmm
 
 struct fmm_plan_s {
@@ -152,6 +174,12 @@ struct fmm_plan_s {
   fmm::DevBuf<int32_t> flags;
   fmm::DevBuf<double> host_stage_q, host_stage_phi, host_stage_grad;  // fmm_matvec_host buffers
 
+  // multi-GPU LET exchange (let.cu)
+  fmm::LetLists let;
+  fmm::LetDev let_dev;
+  bool let_ready = false;
+  bool near_compact_out = false;  // near field writes owned results in Morton order (LET)
+
   double t_setup[8] = {0};
   double t_matvec[8] = {0};
   cudaEvent_t ev[8] = {nullptr};
@@ -165,6 +193,7 @@ void build_tree(fmm_plan_s& P, const double* xyz);
 void traverse(fmm_plan_s& P);
 // matvec stages (expansions.cu, near.cu)
 void upward(fmm_plan_s& P);
+void upward_own(fmm_plan_s& P);  // P2M of this rank's leaves only, then M2M (LET)
 void m2l_pass(fmm_plan_s& P);
 void m2l_dmma_setup(fmm_plan_s& P);
 void m2l_dmma_pass(fmm_plan_s& P);
@@ -176,6 +205,17 @@ void downward(fmm_plan_s& P);
 void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
 void near_pass_warp(fmm_plan_s& P, double* phi, double* grad);
 void gather_charges(fmm_plan_s& P, const double* q);
+std::vector<int64_t> let_cuts(const int32_t* leaf_begin_sorted, int64_t nleaves, int64_t n, int world);
+void let_lists(int64_t n, int world, int me, const int64_t* caller_off, const uint32_t* perm, int64_t ncells,
+               const int32_t* cbeg, const int32_t* cend, int64_t nleaves, const int32_t* leaves, int64_t np2p,
+               const int32_t* p2p_tgt, const int32_t* p2p_src, int64_t nm2l, const int32_t* m2l_tgt,
+               const int32_t* m2l_src, LetLists& out);
+void let_setup(fmm_plan_s& P, const int64_t* caller_counts);
+void let_pack_q(fmm_plan_s& P, const double* q_local, double* send);
+void let_upward(fmm_plan_s& P, const double* q_recv, double* shared_send, double* m_send);
+void let_exchange_in(fmm_plan_s& P, const double* shared_recv, const double* m_recv);
+void let_pack_phi(fmm_plan_s& P, double* phi_send, double* grad_send);
+void let_unpack(fmm_plan_s& P, const double* phi_recv, const double* grad_recv, double* phi, double* grad);
 void launch_direct(const double* src, const double* q, int64_t ns, const double* tgt, int64_t nt,
                    double* phi, double* grad, cudaStream_t s);
 }  // namespace fmm

@@ -106,6 +106,46 @@ class Plan:
         d["t_matvec_ms"] = list(s.t_matvec_ms)
         return d
 
+    # ---- multi-GPU LET exchange (fmm.h fmm_let_*); buffers are device float64 tensors
+    def let_setup(self, caller_counts):
+        cc = (C.c_int64 * len(caller_counts))(*[int(c) for c in caller_counts])
+        N.check(N.lib().fmm_let_setup(self._h, cc))
+        nc = (self.p + 1) * (self.p + 2) // 2
+        self.let = {name: self._let_counts(code) for name, code in (
+            ("q_send", N.FMM_LET_Q_SEND), ("q_recv", N.FMM_LET_Q_RECV), ("m_send", N.FMM_LET_M_SEND),
+            ("m_recv", N.FMM_LET_M_RECV), ("phi_send", N.FMM_LET_PHI_SEND), ("phi_recv", N.FMM_LET_PHI_RECV))}
+        sh = (C.c_int64 * 1)()
+        N.check(N.lib().fmm_let_counts(self._h, N.FMM_LET_SHARED, sh))
+        self.let["shared"] = int(sh[0])
+        rb = (C.c_int64 * (self.world + 1))()
+        N.check(N.lib().fmm_let_counts(self._h, N.FMM_LET_RANK_BEGIN, rb))
+        self.let["rank_begin"] = list(rb)
+        self.let["ncd"] = 2 * nc  # doubles per expansion
+        return self.let
+
+    def _let_counts(self, code):
+        out = (C.c_int64 * self.world)()
+        N.check(N.lib().fmm_let_counts(self._h, code, out))
+        return list(out)
+
+    @staticmethod
+    def _p(t):
+        return C.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else None
+
+    def let_pack_q(self, q_local, q_send):
+        N.check(N.lib().fmm_let_pack_q(self._h, self._p(q_local), self._p(q_send)))
+
+    def let_upward(self, q_recv, shared_send, m_send):
+        N.check(N.lib().fmm_let_upward(self._h, self._p(q_recv), self._p(shared_send), self._p(m_send)))
+
+    def let_finish(self, shared_recv, m_recv, phi_send, grad_send=None):
+        N.check(N.lib().fmm_let_finish(self._h, self._p(shared_recv), self._p(m_recv), self._p(phi_send),
+                                       self._p(grad_send)))
+
+    def let_unpack(self, phi_recv, grad_recv, phi_local, grad_local=None):
+        N.check(N.lib().fmm_let_unpack(self._h, self._p(phi_recv), self._p(grad_recv), self._p(phi_local),
+                                       self._p(grad_local)))
+
     _EXPORT = {
         "keys": (N.FMM_X_KEYS, np.uint64, None), "perm": (N.FMM_X_PERM, np.uint32, None),
         "level": (N.FMM_X_LEVEL, np.int32, None), "anchor": (N.FMM_X_ANCHOR, np.int32, 3),
@@ -141,6 +181,27 @@ def direct(src: torch.Tensor, q: torch.Tensor, tgt: torch.Tensor | None = None, 
                                C.c_void_p(tgt.data_ptr()), nt, C.c_void_p(phi.data_ptr()),
                                C.c_void_p(g.data_ptr()) if g is not None else None, C.byref(ex)))
     return (phi, g) if grad else phi
+
+
+def let_lists_host(n, world, me, caller_off, perm, cbeg, cend, leaves, p2p, m2l, what):
+    """Host-only exchange-list builder (fmm_let_lists_host; no device work): numpy arrays in, one list out."""
+    import numpy as _np
+
+    def a(x, dt):
+        return _np.ascontiguousarray(x, dtype=dt)
+
+    co, pm = a(caller_off, _np.int64), a(perm, _np.uint32)
+    cb, ce, lv = a(cbeg, _np.int32), a(cend, _np.int32), a(leaves, _np.int32)
+    pt, ps = a(p2p[:, 0], _np.int32), a(p2p[:, 1], _np.int32)
+    mt, ms = a(m2l[:, 0], _np.int32), a(m2l[:, 1], _np.int32)
+    ptr = lambda x: C.c_void_p(x.ctypes.data)  # noqa: E731
+    args = [int(n), int(world), int(me), ptr(co), ptr(pm), len(cb), ptr(cb), ptr(ce), len(lv), ptr(lv), len(pt),
+            ptr(pt), ptr(ps), len(mt), ptr(mt), ptr(ms), int(what)]
+    cnt = C.c_int64()
+    N.check(N.lib().fmm_let_lists_host(*args, None, 0, C.byref(cnt)))
+    out = _np.empty(cnt.value, dtype=_np.int64)
+    N.check(N.lib().fmm_let_lists_host(*args, C.c_void_p(out.ctypes.data), cnt.value, C.byref(cnt)))
+    return out
 
 
 def version() -> str:

@@ -1,10 +1,9 @@
-"""Multi-process (world_size 2, gloo, CPU) tests of the multi-GPU host logic in
-paper_1602_02244_b200/dist.py: the collectives only move bytes,
-so they run unchanged on CPU tensors. The per-rank compute is a test double
-(`_OwnRangeDirect`) that mimics libfmm's contract for world > 1: each rank
-returns exact values for the targets it owns and exact zeros elsewhere, so
-the reduce-scatter reassembles the global result in every caller's slice.
-The CUDA mat-vec itself is covered by the -m gpu tests.
+"""Multi-process (world_size 2, gloo, CPU) tests of the collective helpers in
+paper_1602_02244_b200/dist.py: they only move bytes, so they run
+unchanged on CPU tensors. The whole LET protocol over gloo is in tests/test_let.py;
+the CUDA mat-vec itself is covered by the -m gpu tests. `_OwnRangeDirect` is a
+test double for the replicated mode of fmm_matvec (world > 1, global q): exact
+values for the owned targets, zeros elsewhere, reassembled by scatter_sum.
 """
 import os
 import socket
@@ -56,7 +55,7 @@ def _worker(rank, world, port, n, counts, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1602_02244_b200.dist import DistributedPlan, gather_counts, gather_rows, scatter_sum
+        from paper_1602_02244_b200.dist import all_to_all_v, gather_counts, gather_rows, scatter_sum
 
         x, q = F.cube(n, seed=3)
         offs = np.concatenate([[0], np.cumsum(counts)])
@@ -71,9 +70,19 @@ def _worker(rank, world, port, n, counts, out):
         contrib[rank::world] = torch.arange(n, dtype=torch.float64)[rank::world]
         s = scatter_sum(contrib, list(counts), rank)
         assert torch.equal(s, torch.arange(n, dtype=torch.float64)[lo:hi])
-        plan = DistributedPlan(xl, 4, 8, 0.4, plan_factory=_OwnRangeDirect)
-        phi, g = plan.matvec(ql, grad=True)
-        out[rank] = (phi.numpy().copy(), g.numpy().copy())
+        # replicated mode: every rank evaluates its owned targets of the global q, scatter_sum reassembles
+        plan = _OwnRangeDirect(xa, 4, 8, 0.4, rank=rank, world=world)
+        phi, g = plan.matvec(gather_rows(ql, list(counts)), grad=True)
+        phi_l = scatter_sum(phi, list(counts), rank)
+        g_l = scatter_sum(g, list(counts), rank)
+        out[rank] = (phi_l.numpy().copy(), g_l.numpy().copy())
+        # uneven all-to-all of rows (width 3): rank r sends (r + 1) * (d + 1) rows to d
+        sc = [(rank + 1) * (d + 1) for d in range(world)]
+        rc = [(r + 1) * (rank + 1) for r in range(world)]
+        send = torch.cat([torch.full((c * 3,), 100.0 * rank + d, dtype=torch.float64) for d, c in enumerate(sc)])
+        recv = all_to_all_v(send, sc, rc, 3)
+        exp = torch.cat([torch.full((c * 3,), 100.0 * r + rank, dtype=torch.float64) for r, c in enumerate(rc)])
+        assert torch.equal(recv, exp)
     finally:
         dist.destroy_process_group()
 

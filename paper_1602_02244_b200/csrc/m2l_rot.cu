@@ -40,6 +40,7 @@
 //  * 4 accumulate warps: add chunk i's result (Az_L and the symmetry map applied on the fly)
 //    into the tile's shared-memory accumulators in column order (deterministic, no atomics).
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -78,7 +79,7 @@ constexpr int rot_xstride(int kpad) {
 // chunk width (columns) of the v3 kernel and its shared-memory budget
 constexpr int rot_nc(int p) { return p <= 10 ? 40 : 32; }
 #ifndef FMM_ROT_MMA
-#define FMM_ROT_MMA 12
+#define FMM_ROT_MMA 8
 #endif
 constexpr int kRotMMA = FMM_ROT_MMA;  // MMA warps of the v3 kernel
 constexpr int rot_ksb(int p) { return (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB)
@@ -260,6 +261,7 @@ struct RotArgs {
   const int32_t* ipos;   // [nitems][2][16] RI positions
   const int32_t* desc;   // [nchunks][rot_desc_ints(NC)] chunk descriptors
   int smax, nitems, blob;
+  unsigned long long* prof;  // timing experiments (dbg & 256): per MMA warp cycles [wait X, stage 0..2, barriers]
 };
 
 template <int P>
@@ -573,13 +575,18 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
     }
   } else {
     // ================= MMA warps: the three block-GEMM stages in place
+    unsigned long long tw = 0, ts[3] = {0, 0, 0}, tb = 0, t0 = 0;
+    const bool prof = (dbg & 256) && r.prof;
     for (int ch = c_first; ch < c_last; ++ch) {
       const int i = ch - c_first, b = i & 1;
+      if (prof) t0 = clock64();
       named_sync(1 + b, nprep_t + nmma_t);  // Xfull(i)
+      if (prof) tw += clock64() - t0;
       double* xc = b ? m.x1 : m.x0;
       const double* ob = m.ob + b * BLOB;
       const int ntiles = (m.desc[(i % 3) * rot_desc_ints(NC)] + 7) >> 3;
       for (int st = 0; st < 3; ++st) {
+        if (prof) t0 = clock64();
         const int32_t* sl = m.sched + (st * G::NMMA + warp) * r.smax;
         for (int k = 0; k < r.smax && !(dbg & 1); ++k) {
           const int id = sl[k];
@@ -594,9 +601,24 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
           else
             rot_item<P, 1, 2>(A, ps, nparts, sgn1, ntiles, xc, lane, dbg);
         }
+        if (prof) {
+          const unsigned long long t1 = clock64();
+          ts[st] += t1 - t0;
+          t0 = t1;
+        }
         if (st < 2 && !(dbg & 16)) named_sync(5, nmma_t);  // stage st complete before st + 1 reads it
+        if (prof) tb += clock64() - t0;
       }
       named_arrive(3 + b, nmma_t + nacc_t);  // Yfull(i)
+    }
+    if (prof && lane == 0) {
+      unsigned long long* o = r.prof + 8 * warp;
+      atomicAdd(o + 0, tw);
+      atomicAdd(o + 1, ts[0]);
+      atomicAdd(o + 2, ts[1]);
+      atomicAdd(o + 3, ts[2]);
+      atomicAdd(o + 4, tb);
+      atomicAdd(o + 5, (unsigned long long)(c_last - c_first));
     }
   }
   __syncthreads();
@@ -896,10 +918,17 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
   r.nitems = D.rot_nitems;
   r.blob = D.rot_blob;
   r.desc = D.rot_desc;
+  const char* dbgs = getenv("FMM_M2L_DEBUG");  // timing experiments only (most bits skip work: wrong results)
+  const int dbg = dbgs ? atoi(dbgs) : 0;
+  r.prof = nullptr;
+  static DevBuf<unsigned long long> prof_buf;
+  if (dbg & 256) {  // timing experiment: per-warp cycle breakdown printed to stderr after the launch
+    if (!prof_buf.ptr) prof_buf.alloc(8 * 32);
+    FMM_CUDA(cudaMemsetAsync(prof_buf.ptr, 0, 8 * 32 * sizeof(unsigned long long), P.stream));
+    r.prof = prof_buf.ptr;
+  }
   const size_t sh = rot_smem_bytes(P.p, a.T, D.rot_smax);
   void (*k)(const RotArgs, int) = nullptr;
-  const char* dbgs = getenv("FMM_M2L_DEBUG");  // timing experiments only (skips work: wrong results)
-  const int dbg = dbgs ? atoi(dbgs) : 0;
   switch (P.p) {
     case 5: k = m2l_rot_kernel<5>; break;
     case 6: k = m2l_rot_kernel<6>; break;
@@ -919,6 +948,15 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
   }
   k<<<(unsigned)D.ntiles, 32 * (kRotMMA + 4 + 8), sh, P.stream>>>(r, dbg);
   FMM_LAUNCHED("m2l_rot_kernel");
+  if (dbg & 256) {
+    unsigned long long h[8 * 32];
+    FMM_CUDA(cudaMemcpyAsync(h, prof_buf.ptr, sizeof(h), cudaMemcpyDeviceToHost, P.stream));
+    FMM_CUDA(cudaStreamSynchronize(P.stream));
+    for (int w = 0; w < kRotMMA; ++w)
+      fprintf(stderr, "m2l_rot prof warp %2d: waitX %.0f  st0 %.0f  st1 %.0f  st2 %.0f  barrier %.0f  (cycles per chunk)\n",
+              w, (double)h[8 * w] / h[8 * w + 5], (double)h[8 * w + 1] / h[8 * w + 5], (double)h[8 * w + 2] / h[8 * w + 5],
+              (double)h[8 * w + 3] / h[8 * w + 5], (double)h[8 * w + 4] / h[8 * w + 5]);
+  }
 }
 
 }  // namespace fmm

@@ -16,41 +16,116 @@ namespace fmm {
 namespace {
 
 constexpr int kExpThreads = 128;  // >= ncoef(p) for p <= 14; two outputs per thread up to p = 21
-constexpr int kP2MChunk = 32;     // particles whose harmonics are staged per round
 constexpr int kM2MThreads = 256;  // M2M / L2L: items (child, coefficient)
 
-// S7 P2M: M_n^m(c) = sum_i q_i conj R_n^m(x_i - c), one block per leaf; the harmonics
-// of a chunk of particles are computed column-parallel (item = (particle, m)).
-__global__ void p2m_kernel(const int32_t* __restrict__ leaves, const int32_t* __restrict__ cbeg,
-                           const int32_t* __restrict__ cend, const double4* __restrict__ center,
-                           const double4* __restrict__ pos, int p, int nc, double2* __restrict__ M) {
-  extern __shared__ double2 shR[];  // [kP2MChunk][nc], rows hold q * conj(R)
-  const int leaf = leaves[blockIdx.x];
+// S7 P2M, warp per leaf: for each order m the column R_n^m (n = m..p) of every particle is
+// generated in registers (diagonal product + two-term recurrence), q conj(R) accumulated per
+// lane over the leaf's particles (lane = particle), then butterfly-reduced over the warp in
+// a fixed order (deterministic); lane k writes coefficient (m + k, m).
+constexpr int kP2MWarps = 4;
+constexpr int kP2MCache = 2;  // particles per lane kept in registers (leaves of <= 64 particles)
+
+// one particle's column m contribution: acc[k] += q conj(R_{m+k}^m), given d = R_m^m
+template <int P>
+__device__ __forceinline__ void p2m_column(double2 (&acc)[P + 1], int m, double2 d, double x, double y, double z,
+                                           double q) {
+  const double r2 = x * x + y * y + z * z;
+  double2 a = d, bb = cscale(d, z);
+  acc[0].x = fma(q, a.x, acc[0].x);
+  acc[0].y = fma(-q, a.y, acc[0].y);
+#pragma unroll
+  for (int k = 1; k <= P; ++k) {
+    if (m + k > P) break;
+    if (k >= 2) {
+      const int n = m + k;
+      const double inv = c_inv_nm.v[n * (kMaxP + 1) + m];
+      const double2 cc = make_double2(((2 * n - 1) * z * bb.x - r2 * a.x) * inv, ((2 * n - 1) * z * bb.y - r2 * a.y) * inv);
+      a = bb;
+      bb = cc;
+    }
+    acc[k].x = fma(q, bb.x, acc[k].x);
+    acc[k].y = fma(-q, bb.y, acc[k].y);
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * kP2MWarps) p2m_warp_kernel(const int32_t* __restrict__ leaves, int64_t nleaves,
+                                                                 const int32_t* __restrict__ cbeg,
+                                                                 const int32_t* __restrict__ cend,
+                                                                 const double4* __restrict__ center,
+                                                                 const double4* __restrict__ pos, int nc,
+                                                                 double2* __restrict__ M) {
+  constexpr int kStride = 2 * (P + 1) + 1;  // odd stride: row writes and column reads conflict-free
+  __shared__ double red[kP2MWarps][32 * kStride];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t li = (int64_t)blockIdx.x * kP2MWarps + w;
+  if (li >= nleaves) return;  // warp-uniform; only __syncwarp below
+  const int leaf = leaves[li];
   const int32_t b = cbeg[leaf], e = cend[leaf];
   const double4 c = center[leaf];
-  const int t0 = threadIdx.x, t1 = threadIdx.x + kExpThreads;
-  double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
-  for (int32_t s0 = b; s0 < e; s0 += kP2MChunk) {
-    const int cnt = min(kP2MChunk, e - s0);
-    for (int it = threadIdx.x; it < cnt * (p + 1); it += blockDim.x) {
-      const int i = it / (p + 1), m = it - i * (p + 1);
-      const double4 x = pos[s0 + i];
-      double2* R = shR + i * nc;
-      regular_column(x.x - c.x, x.y - c.y, x.z - c.z, m, p, R);
-      for (int n = m; n <= p; ++n) {
-        const double2 v = R[cidx(n, m)];
-        R[cidx(n, m)] = make_double2(x.w * v.x, -x.w * v.y);
-      }
-    }
-    __syncthreads();
-    for (int k = 0; k < cnt; ++k) {
-      if (t0 < nc) a0 = cadd(a0, shR[k * nc + t0]);
-      if (t1 < nc) a1 = cadd(a1, shR[k * nc + t1]);
-    }
-    __syncthreads();
+  double* Ml = (double*)(M + (int64_t)leaf * nc);
+  double* rw = red[w];
+  // the lane's first kP2MCache particles: relative coordinates, charge, running diagonal R_m^m
+  double px[kP2MCache], py[kP2MCache], pz[kP2MCache], pq[kP2MCache];
+  double2 dg[kP2MCache];
+#pragma unroll
+  for (int u = 0; u < kP2MCache; ++u) {
+    const int32_t i = b + lane + 32 * u;
+    const double4 v = i < e ? pos[i] : make_double4(c.x, c.y, c.z, 0.0);
+    px[u] = v.x - c.x;
+    py[u] = v.y - c.y;
+    pz[u] = v.z - c.z;
+    pq[u] = v.w;
+    dg[u] = make_double2(1.0, 0.0);
   }
-  if (t0 < nc) M[(int64_t)leaf * nc + t0] = a0;
-  if (t1 < nc) M[(int64_t)leaf * nc + t1] = a1;
+  for (int m = 0; m <= P; ++m) {
+    const int len = P + 1 - m;  // column (n = m..p) of complex values
+    double2 acc[P + 1];
+#pragma unroll
+    for (int k = 0; k <= P; ++k) acc[k] = make_double2(0.0, 0.0);
+    if (m > 0) {
+      const double s = c_half_inv.v[m];
+#pragma unroll
+      for (int u = 0; u < kP2MCache; ++u) dg[u] = cmul(dg[u], make_double2(s * px[u], s * py[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < kP2MCache; ++u) p2m_column<P>(acc, m, dg[u], px[u], py[u], pz[u], pq[u]);
+    for (int32_t i = b + lane + 32 * kP2MCache; i < e; i += 32) {  // leaves larger than 32 kP2MCache
+      const double4 v = pos[i];
+      const double x = v.x - c.x, y = v.y - c.y, z = v.z - c.z;
+      double2 d = make_double2(1.0, 0.0);
+      for (int k = 1; k <= m; ++k) {
+        const double s = c_half_inv.v[k];
+        d = cmul(d, make_double2(s * x, s * y));
+      }
+      p2m_column<P>(acc, m, d, x, y, z, v.w);
+    }
+    // transpose through shared memory: lane t sums value t of the column over the 32 lanes
+#pragma unroll
+    for (int k = 0; k <= P; ++k) {
+      if (k >= len) break;
+      rw[lane * kStride + 2 * k] = acc[k].x;
+      rw[lane * kStride + 2 * k + 1] = acc[k].y;
+    }
+    __syncwarp();
+    if (lane < 2 * len) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+      for (int r = 0; r < 32; r += 2) {
+        s0 += rw[r * kStride + lane];
+        s1 += rw[(r + 1) * kStride + lane];
+      }
+      Ml[2 * cidx(m + (lane >> 1), m) + (lane & 1)] = s0 + s1;
+    }
+    __syncwarp();
+  }
+}
+
+template <int P>
+void launch_p2m(fmm_plan_s& P_, const int32_t* leaves, int64_t nl, cudaStream_t s) {
+  p2m_warp_kernel<P><<<cdiv(nl, kP2MWarps), 32 * kP2MWarps, 0, s>>>(leaves, nl, P_.cells.begin, P_.cells.end,
+                                                                   P_.cells.center, P_.pos, P_.nc, P_.M);
+  FMM_LAUNCHED("p2m_warp_kernel");
 }
 
 // M2M term for output (j, k): sum_{n<=j} sum_m conj R_n^m(c - c') M_{j-n}^{k-m}(c)
@@ -186,11 +261,27 @@ void upward_impl(fmm_plan_s& P, int64_t leaf_b, int64_t leaf_e) {
   cudaStream_t s = P.stream;
   const int nc = P.nc;
   if (leaf_e > leaf_b) {
-    const size_t sh = sizeof(double2) * kP2MChunk * nc;
-    if (sh > 48 * 1024) FMM_CUDA(cudaFuncSetAttribute(p2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    p2m_kernel<<<(unsigned)(leaf_e - leaf_b), kExpThreads, sh, s>>>(
-        P.leaves.ptr + leaf_b, P.cells.begin, P.cells.end, P.cells.center, P.pos, P.p, nc, P.M);
-    FMM_LAUNCHED("p2m_kernel");
+    const int64_t nl = leaf_e - leaf_b;
+    const int32_t* lv = P.leaves.ptr + leaf_b;
+    switch (P.p) {
+      case 0: launch_p2m<0>(P, lv, nl, s); break;
+      case 1: launch_p2m<1>(P, lv, nl, s); break;
+      case 2: launch_p2m<2>(P, lv, nl, s); break;
+      case 3: launch_p2m<3>(P, lv, nl, s); break;
+      case 4: launch_p2m<4>(P, lv, nl, s); break;
+      case 5: launch_p2m<5>(P, lv, nl, s); break;
+      case 6: launch_p2m<6>(P, lv, nl, s); break;
+      case 7: launch_p2m<7>(P, lv, nl, s); break;
+      case 8: launch_p2m<8>(P, lv, nl, s); break;
+      case 9: launch_p2m<9>(P, lv, nl, s); break;
+      case 10: launch_p2m<10>(P, lv, nl, s); break;
+      case 11: launch_p2m<11>(P, lv, nl, s); break;
+      case 12: launch_p2m<12>(P, lv, nl, s); break;
+      case 13: launch_p2m<13>(P, lv, nl, s); break;
+      case 14: launch_p2m<14>(P, lv, nl, s); break;
+      case 15: launch_p2m<15>(P, lv, nl, s); break;
+      default: launch_p2m<16>(P, lv, nl, s); break;
+    }
   }
   const size_t sh = sizeof(double2) * 24 * nc;
   static size_t configured = 0;

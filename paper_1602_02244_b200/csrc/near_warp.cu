@@ -123,15 +123,32 @@ __device__ void process_group(const NearArgs& a, int leaf, int t0, int cnt, int 
     f[k] = 0.0;
     g[k] = make_double3(0, 0, 0);
   }
-  const int q1 = a.off[leaf + 1];
+  const int q0 = a.off[leaf], q1 = a.off[leaf + 1];
+  // the first 32 list entries' source ranges, one per lane, loaded once (no dependent
+  // global loads on the staging path); later entries are read when needed
+  int my_sl = -1, my_b = 0, my_e = 0;
+  if (q0 + lane < q1) {
+    my_sl = a.src[q0 + lane];
+    my_b = a.cbeg[my_sl];
+    my_e = a.cend[my_sl];
+  }
   // Build and issue (cp.async) the unit starting at (qa, off) into buffer b.
   auto stage = [&](int qa, int off, int b) -> Unit {
     Unit u{qa, qa, off, 0, false};
     double* dst = (double*)buf[b];
     for (int q = qa; q < q1; ++q) {
-      const int sl = a.src[q];
-      const int sb = a.cbeg[sl] + (q == qa ? off : 0);
-      const int sz = a.cend[sl] - sb;
+      int sl, sb0, se;
+      if (q - q0 < 32) {
+        sl = __shfl_sync(0xffffffffu, my_sl, q - q0);
+        sb0 = __shfl_sync(0xffffffffu, my_b, q - q0);
+        se = __shfl_sync(0xffffffffu, my_e, q - q0);
+      } else {
+        sl = a.src[q];
+        sb0 = a.cbeg[sl];
+        se = a.cend[sl];
+      }
+      const int sb = sb0 + (q == qa ? off : 0);
+      const int sz = se - sb;
       const bool self = sl == leaf;
       if (q > qa && (self || sz > kBuf - u.n)) break;  // the unit is full / the self leaf goes alone
       const int n = min(kBuf - u.n, sz);
@@ -152,7 +169,7 @@ __device__ void process_group(const NearArgs& a, int leaf, int t0, int cnt, int 
     if (u.qb == u.qa) return make_int2(u.qa, u.off + u.n);  // partial oversized leaf
     return make_int2(u.qb, 0);
   };
-  int qa = a.off[leaf], off = 0, b = 0;
+  int qa = q0, off = 0, b = 0;
   if (qa < q1) {
     Unit u = stage(qa, off, 0);
     while (true) {

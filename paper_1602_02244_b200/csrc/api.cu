@@ -126,6 +126,10 @@ void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
   T.mark(0);
   fmm::gather_charges(P, q);
   fmm::upward(P);
+  // near field fused into the M2L v3 kernel (P2P warps on the FP64 pipe)
+  P.near_fused_active = P.fuse_near && P.m2l_variant == 3 && P.near_variant == 2 && P.m2l_dmma.ntiles > 0;
+  P.near_fused_grad = grad != nullptr;
+  if (P.near_fused_active) fmm::near_fused_prepare(P, grad != nullptr);
   T.mark(1);
   if (P.m2l_variant >= 2)
     fmm::m2l_dmma_pass(P);
@@ -138,10 +142,13 @@ void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
     FMM_CUDA(cudaMemsetAsync(phi, 0, sizeof(double) * P.n, P.stream));
     if (grad) FMM_CUDA(cudaMemsetAsync(grad, 0, sizeof(double) * 3 * P.n, P.stream));
   }
-  if (P.near_variant == 2)
+  if (P.near_fused_active)
+    fmm::near_fused_finish(P, phi, grad);
+  else if (P.near_variant == 2)
     fmm::near_pass_warp(P, phi, grad);
   else
     fmm::near_pass(P, q, phi, grad);
+  P.near_fused_active = false;
   T.mark(4);
   if (T.on) {
     FMM_CUDA(cudaEventSynchronize(P.ev[4]));
@@ -219,6 +226,8 @@ fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncr
     if (v && v[0] >= '1' && v[0] <= '3') P->m2l_variant = v[0] - '0';
     const char* nv = getenv("FMM_NEAR_VARIANT");
     if (nv && nv[0] == '1') P->near_variant = 1;
+    const char* fz = getenv("FMM_FUSE_NEAR");  // experiment: P2P warps inside the M2L v3 kernel
+    P->fuse_near = fz && fz[0] == '1';
     const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // test hook: export M2L-only local expansions
     P->debug_skip_l2l = dbg && dbg[0] == '1';
     if (P->m2l_variant >= 2) fmm::m2l_dmma_setup(*P);
@@ -493,6 +502,9 @@ fmm_status fmm_let_finish(fmm_plan P, const double* shared_recv, const double* m
     Timer T(*P, P->timing);
     T.mark(1);
     fmm::let_exchange_in(*P, shared_recv, m_recv);
+    P->near_fused_active = P->fuse_near && P->m2l_variant == 3 && P->near_variant == 2 && P->m2l_dmma.ntiles > 0;
+    P->near_fused_grad = grad_send != nullptr;
+    if (P->near_fused_active) fmm::near_fused_prepare(*P, grad_send != nullptr);
     if (P->m2l_variant >= 2)
       fmm::m2l_dmma_pass(*P);
     else
@@ -501,8 +513,12 @@ fmm_status fmm_let_finish(fmm_plan P, const double* shared_recv, const double* m
     fmm::downward(*P);
     T.mark(3);
     P->near_compact_out = true;
-    fmm::near_pass_warp(*P, P->let_dev.phi_own.ptr, grad_send ? P->let_dev.grad_own.ptr : nullptr);
+    if (P->near_fused_active)
+      fmm::near_fused_finish(*P, P->let_dev.phi_own.ptr, grad_send ? P->let_dev.grad_own.ptr : nullptr);
+    else
+      fmm::near_pass_warp(*P, P->let_dev.phi_own.ptr, grad_send ? P->let_dev.grad_own.ptr : nullptr);
     P->near_compact_out = false;
+    P->near_fused_active = false;
     fmm::let_pack_phi(*P, phi_send, grad_send);
     T.mark(4);
     if (T.on) {

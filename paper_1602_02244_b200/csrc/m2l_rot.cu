@@ -47,6 +47,7 @@
 
 #include "harmonics.cuh"
 #include "m2l_common.cuh"
+#include "near_common.cuh"
 #include "plan.h"
 
 namespace fmm {
@@ -82,6 +83,14 @@ constexpr int rot_nc(int p) { return p <= 10 ? 40 : 32; }
 #define FMM_ROT_MMA 8
 #endif
 constexpr int kRotMMA = FMM_ROT_MMA;  // MMA warps of the v3 kernel
+#ifndef FMM_ROT_ACC
+#define FMM_ROT_ACC 8
+#endif
+#ifndef FMM_ROT_NEAR
+#define FMM_ROT_NEAR 0
+#endif
+constexpr int kRotAcc = FMM_ROT_ACC;    // accumulate warps
+constexpr int kRotNear = FMM_ROT_NEAR;  // near-field (P2P) warps fused into the kernel
 constexpr int rot_ksb(int p) { return (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB)
 // ints of one per-chunk descriptor: [ncol, nseg, class, 0 | srcs | meta | sslot | sbeg[NC + 1]]
 constexpr int rot_desc_ints(int nc) { return (4 + 4 * nc + 1 + 3) & ~3; }
@@ -261,6 +270,12 @@ struct RotArgs {
   const int32_t* ipos;   // [nitems][2][16] RI positions
   const int32_t* desc;   // [nchunks][rot_desc_ints(NC)] chunk descriptors
   int smax, nitems, blob;
+  // fused near field (P2P on the FP64 pipe while the MMA warps use the DMMA pipe); p2p_phi null = off
+  const int32_t *leaves, *cbeg, *cend, *p2p_off, *p2p_src;
+  const double4* pos;
+  int64_t nleaves;
+  int* leaf_counter;
+  double *p2p_phi, *p2p_grad;
   unsigned long long* prof;  // timing experiments (dbg & 256): per MMA warp cycles [wait X, stage 0..2, barriers]
 };
 
@@ -271,7 +286,7 @@ struct RGeo {
   static constexpr int S = rot_xstride(KPAD);  // column stride (see col_base)
   static constexpr int NC = rot_nc(P);
   static constexpr int NT = NC / 8;
-  static constexpr int NMMA = kRotMMA, NPREP = 4, NACC = 8;
+  static constexpr int NMMA = kRotMMA, NPREP = 4, NACC = kRotAcc, NNEAR = kRotNear;
   static constexpr int KSB = rot_ksb(P);
   static constexpr int NCOEF = (P + 1) * (P + 2) / 2;
 };
@@ -283,6 +298,7 @@ struct RotSmem {
   int32_t *dec, *pairtab, *sched, *ihdr, *ipos;
   int2* colt;                  // [2][NC] per buffer: (column base, 2 g) of each chunk column
   uint32_t *mmask, *lmask;     // [NR] symmetry masks (bit 2g: take re/im partner, 2g+1: negate)
+  int* flag;                   // MMA warps done (near warps stop)
 };
 template <int P>
 __device__ __forceinline__ RotSmem rot_carve(double* sm, const RotArgs& r) {
@@ -300,7 +316,8 @@ __device__ __forceinline__ RotSmem rot_carve(double* sm, const RotArgs& r) {
   m.lmask = m.mmask + G::NR;
   m.pairtab = (int32_t*)(m.lmask + G::NR);
   m.colt = (int2*)(((uintptr_t)(m.pairtab + G::NCOEF) + 7) & ~(uintptr_t)7);
-  m.ihdr = (int32_t*)(m.colt + 2 * G::NC);
+  m.flag = (int*)(m.colt + 2 * G::NC);
+  m.ihdr = m.flag + 2;
   m.ipos = m.ihdr + r.nitems;
   m.sched = m.ipos + 32 * r.nitems;
   return m;
@@ -406,7 +423,7 @@ __device__ __forceinline__ void rot_item(const double* __restrict__ A, const int
 // Named barriers: 1/2 Xfull(b) prep -> MMA; 3/4 Yfull(b) MMA -> acc; 7/8 Xfree(b) acc -> prep;
 // 5 MMA warps (between stages); 6 prep warps.
 template <int P>
-__global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>::NACC), 1)
+__global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>::NACC + RGeo<P>::NNEAR), 1)
     m2l_rot_kernel(const RotArgs r, int dbg) {
   using G = RGeo<P>;
   constexpr int NR = G::NR, NC = G::NC, S = G::S, NCOEF = G::NCOEF;
@@ -435,12 +452,30 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
     m.lmask[q] = r.masks[NR + q];
   }
   if (tid == 0) {
+    *m.flag = 0;
     for (int j = 0; j < 5; ++j) mbar_init(m.bar + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int c_first = a.tile_chunk[tile], c_last = a.tile_chunk[tile + 1];
   __syncthreads();
-  if (warp >= G::NMMA + G::NPREP) {
+  if (warp >= G::NMMA + G::NPREP + G::NACC) {
+    // ================= near warps: P2P of own leaves (global leaf counter) until the MMA warps are done
+    if (r.p2p_phi && !(dbg & 512)) {
+      while (true) {
+        if (*(volatile int*)m.flag) break;
+        int li = 0;
+        if (lane == 0) li = atomicAdd(r.leaf_counter, 1);
+        li = __shfl_sync(0xffffffffu, li, 0);
+        if (li >= r.nleaves) break;
+        if (r.p2p_grad)
+          near::p2p_leaf_global<true, 2>(r.cbeg, r.cend, r.p2p_off, r.p2p_src, r.pos, r.leaves[li], lane, r.p2p_phi,
+                                         r.p2p_grad);
+        else
+          near::p2p_leaf_global<false, 2>(r.cbeg, r.cend, r.p2p_off, r.p2p_src, r.pos, r.leaves[li], lane,
+                                          r.p2p_phi, nullptr);
+      }
+    }
+  } else if (warp >= G::NMMA + G::NPREP) {
     // ================= accumulate warps: acc[slot][r] += (D^L_g Az_L Y)[r] for chunk i
     const int h = tid - nmma_t - nprep_t;
     for (int ch = c_first; ch < c_last; ++ch) {
@@ -611,6 +646,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       }
       named_arrive(3 + b, nmma_t + nacc_t);  // Yfull(i)
     }
+    if (warp == 0 && lane == 0) *(volatile int*)m.flag = 1;  // near warps stop taking leaves
     if (prof && lane == 0) {
       unsigned long long* o = r.prof + 8 * warp;
       atomicAdd(o + 0, tw);
@@ -787,7 +823,7 @@ size_t rot_smem_bytes(int p, int T, int extra_ints) {
   std::vector<RotItem> items = build_items(p, blob);
   const int ni = (int)items.size();
   return sizeof(double) * ((size_t)T * NR + 2 * (size_t)NC * S + 2 * (size_t)blob) + sizeof(uint64_t) * 6 +
-         sizeof(int32_t) * (3 * rot_desc_ints(NC) + 3 * NR + nc + 2 + 4 * NC + ni + 32 * ni + 3 * kRotMMA * extra_ints);
+         sizeof(int32_t) * (3 * rot_desc_ints(NC) + 3 * NR + nc + 4 + 4 * NC + ni + 32 * ni + 3 * kRotMMA * extra_ints);
 }
 
 void m2l_rot_setup(fmm_plan_s& P) {
@@ -918,6 +954,20 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
   r.nitems = D.rot_nitems;
   r.blob = D.rot_blob;
   r.desc = D.rot_desc;
+  r.p2p_phi = nullptr;
+  r.p2p_grad = nullptr;
+  if (P.near_fused_active) {
+    r.leaves = P.leaves.ptr + P.own_leaf_begin;
+    r.nleaves = P.own_leaf_end - P.own_leaf_begin;
+    r.cbeg = P.cells.begin;
+    r.cend = P.cells.end;
+    r.p2p_off = P.p2p.off;
+    r.p2p_src = P.p2p.src;
+    r.pos = P.pos;
+    r.leaf_counter = P.near_counter;
+    r.p2p_phi = P.near_p2p_phi;
+    r.p2p_grad = P.near_fused_grad ? P.near_p2p_grad.ptr : nullptr;
+  }
   const char* dbgs = getenv("FMM_M2L_DEBUG");  // timing experiments only (most bits skip work: wrong results)
   const int dbg = dbgs ? atoi(dbgs) : 0;
   r.prof = nullptr;
@@ -946,7 +996,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
     FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     configured[P.p] = sh;
   }
-  k<<<(unsigned)D.ntiles, 32 * (kRotMMA + 4 + 8), sh, P.stream>>>(r, dbg);
+  k<<<(unsigned)D.ntiles, 32 * (kRotMMA + 4 + kRotAcc + kRotNear), sh, P.stream>>>(r, dbg);
   FMM_LAUNCHED("m2l_rot_kernel");
   if (dbg & 256) {
     unsigned long long h[8 * 32];

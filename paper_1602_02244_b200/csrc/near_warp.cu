@@ -22,10 +22,12 @@
 #include <cstdlib>
 
 #include "harmonics.cuh"
+#include "near_common.cuh"
 #include "plan.h"
 
 namespace fmm {
 namespace {
+using namespace near;
 
 constexpr int kWarps = 4;   // warps (target leaves) per CTA
 constexpr int kBuf = 128;   // source particles per staging buffer
@@ -35,18 +37,6 @@ constexpr int max_tpl() { return kMaxTPL; }
 #ifndef FMM_NEAR_MINB
 #define FMM_NEAR_MINB 4  // CTAs per SM for the phi-only kernel (122 registers, no spills)
 #endif
-#ifndef FMM_NEAR_UNROLL
-#define FMM_NEAR_UNROLL 2
-#endif
-constexpr int kUnroll = FMM_NEAR_UNROLL;
-
-__device__ __forceinline__ double rsqrt_fp64(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double e = fma(-x * y, y, 1.0);     // 1 - x y^2
-  const double c = e * fma(e, 0.375, 0.5);  // e/2 + 3 e^2/8
-  return fma(y, c, y);
-}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -64,32 +54,6 @@ struct Unit {
   int qa, qb, off, n;
   bool self;
 };
-
-template <bool kGrad, bool kCheck, int TPL>
-__device__ __forceinline__ void interact(const double4* __restrict__ sb, int ns, int sg, int G,
-                                         const double3 (&xi)[TPL], double (&f)[TPL], double3 (&g)[TPL]) {
-#pragma unroll kUnroll
-  for (int j = sg; j < ns; j += G) {
-    const double4 s = sb[j];
-#pragma unroll
-    for (int k = 0; k < TPL; ++k) {
-      const double dx = xi[k].x - s.x, dy = xi[k].y - s.y, dz = xi[k].z - s.z;
-      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      double y = rsqrt_fp64(r2);
-      if (kCheck) y = r2 > 0.0 ? y : 0.0;
-      if (!kGrad) {
-        f[k] = fma(s.w, y, f[k]);
-      } else {
-        const double qy = s.w * y;
-        f[k] += qy;
-        const double w = qy * y * y;
-        g[k].x = fma(-w, dx, g[k].x);
-        g[k].y = fma(-w, dy, g[k].y);
-        g[k].z = fma(-w, dz, g[k].z);
-      }
-    }
-  }
-}
 
 struct NearArgs {
   const int32_t* cbeg;
@@ -233,25 +197,6 @@ __device__ void process_group(const NearArgs& a, int leaf, int t0, int cnt, int 
   }
 }
 
-// (G, TPL) minimising the idle slots (32 / G) * TPL - cnt; ties prefer TPL >= G (balanced
-// L2P), then larger TPL (more register reuse of each staged source). TPL == 0: none fits.
-template <bool kGrad>
-__device__ __forceinline__ void choose_layout(int cnt, int maxT, int maxG, int& G, int& TPL) {
-  int best = 1 << 30;
-  G = 1;
-  TPL = 0;
-  for (int g = 8; g >= 1; g >>= 1) {
-    const int per = 32 / g, t = (cnt + per - 1) / per;
-    if (t > maxT || g > maxG) continue;
-    const int key = (per * t) * 4 + (t >= g ? 0 : 2) + (t > TPL ? 0 : 1);
-    if (key < best) {
-      best = key;
-      G = g;
-      TPL = t;
-    }
-  }
-}
-
 template <bool kGrad>
 __device__ __forceinline__ void dispatch(const NearArgs& a, int leaf, int t0, int cnt, int G, int TPL, int lane,
                                          double4 (*buf)[kBuf]) {
@@ -273,7 +218,7 @@ __global__ void __launch_bounds__(32 * kWarps, kGrad ? 3 : FMM_NEAR_MINB) near_w
   const int leaf = leaves[li];
   const int tb = a.cbeg[leaf], te = a.cend[leaf];
   int G, TPL;
-  choose_layout<kGrad>(te - tb, a.max_tpl, a.max_g, G, TPL);
+  choose_layout(te - tb, a.max_tpl, a.max_g, G, TPL);
   if (TPL > 0) {
     dispatch<kGrad>(a, leaf, tb, te - tb, G, TPL, lane, buf[warp]);
   } else {  // more than 32 * kMaxTPL targets: groups of 32 * kMaxTPL, one lane per target
@@ -282,7 +227,90 @@ __global__ void __launch_bounds__(32 * kWarps, kGrad ? 3 : FMM_NEAR_MINB) near_w
   }
 }
 
+// P2P of the leaves not yet taken by the near warps fused into the M2L kernel: warps pull
+// leaf indices from the same counter; results (unscaled, sorted order) to phi / grad.
+template <bool kGrad>
+__global__ void __launch_bounds__(128) p2p_tail_kernel(const int32_t* __restrict__ leaves, int64_t nleaves,
+                                                       int* __restrict__ counter, const int32_t* __restrict__ cbeg,
+                                                       const int32_t* __restrict__ cend, const int32_t* __restrict__ off,
+                                                       const int32_t* __restrict__ src, const double4* __restrict__ pos,
+                                                       double* __restrict__ phi, double* __restrict__ grad) {
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int li = 0;
+    if (lane == 0) li = atomicAdd(counter, 1);
+    li = __shfl_sync(0xffffffffu, li, 0);
+    if (li >= nleaves) return;
+    p2p_leaf_global<kGrad, 4>(cbeg, cend, off, src, pos, leaves[li], lane, phi, grad);
+  }
+}
+
+// L2P (+grad) of every target of the leaves, added to the P2P results, exact 2^-e rescale,
+// scatter to caller order (or owned order, perm == nullptr). Warp per leaf, lane per target.
+template <bool kGrad>
+__global__ void __launch_bounds__(128) l2p_out_kernel(const int32_t* __restrict__ leaves, int64_t nleaves,
+                                                      const int32_t* __restrict__ cbeg, const int32_t* __restrict__ cend,
+                                                      const double4* __restrict__ center,
+                                                      const double4* __restrict__ pos, const double2* __restrict__ L,
+                                                      int p, int nc, const double* __restrict__ p2p_phi,
+                                                      const double* __restrict__ p2p_grad,
+                                                      const uint32_t* __restrict__ perm, int64_t out_base, double s_phi,
+                                                      double s_grad, double* __restrict__ phi_out,
+                                                      double* __restrict__ grad_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t li = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (li >= nleaves) return;
+  const int leaf = leaves[li];
+  const double4 c = center[leaf];
+  const double2* Lc = L + (int64_t)leaf * nc;
+  for (int t = cbeg[leaf] + lane; t < cend[leaf]; t += 32) {
+    const double4 x = pos[t];
+    double f = p2p_phi[t];
+    double3 g = kGrad ? make_double3(p2p_grad[3 * t], p2p_grad[3 * t + 1], p2p_grad[3 * t + 2]) : make_double3(0, 0, 0);
+    l2p_eval<kGrad>(Lc, p, x.x - c.x, x.y - c.y, x.z - c.z, f, g);
+    const int64_t o = perm ? (int64_t)perm[t] : (int64_t)t - out_base;
+    phi_out[o] = f * s_phi;
+    if (kGrad) {
+      grad_out[3 * o] = g.x * s_grad;
+      grad_out[3 * o + 1] = g.y * s_grad;
+      grad_out[3 * o + 2] = g.z * s_grad;
+    }
+  }
+}
+
 }  // namespace
+
+void near_fused_prepare(fmm_plan_s& P, bool grad) {
+  if (P.near_p2p_phi.count < P.n) P.near_p2p_phi.alloc(P.n);
+  if (grad && P.near_p2p_grad.count < 3 * P.n) P.near_p2p_grad.alloc(3 * P.n);
+  if (!P.near_counter.ptr) P.near_counter.alloc(1);
+  FMM_CUDA(cudaMemsetAsync(P.near_counter.ptr, 0, sizeof(int), P.stream));
+}
+
+void near_fused_finish(fmm_plan_s& P, double* phi, double* grad) {
+  const int64_t nl = P.own_leaf_end - P.own_leaf_begin;
+  if (nl <= 0) return;
+  const int32_t* leaves = P.leaves.ptr + P.own_leaf_begin;
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(nl, 4), 148 * 8);
+  if (grad)
+    p2p_tail_kernel<true><<<grid, 128, 0, P.stream>>>(leaves, nl, P.near_counter, P.cells.begin, P.cells.end,
+                                                       P.p2p.off, P.p2p.src, P.pos, P.near_p2p_phi, P.near_p2p_grad);
+  else
+    p2p_tail_kernel<false><<<grid, 128, 0, P.stream>>>(leaves, nl, P.near_counter, P.cells.begin, P.cells.end,
+                                                        P.p2p.off, P.p2p.src, P.pos, P.near_p2p_phi, nullptr);
+  FMM_LAUNCHED("p2p_tail_kernel");
+  const uint32_t* perm = P.near_compact_out ? nullptr : P.perm.ptr;
+  const double s_phi = std::ldexp(1.0, -P.e), s_grad = std::ldexp(1.0, -2 * P.e);
+  if (grad)
+    l2p_out_kernel<true><<<cdiv(nl, 4), 128, 0, P.stream>>>(leaves, nl, P.cells.begin, P.cells.end, P.cells.center,
+                                                            P.pos, P.L, P.p, P.nc, P.near_p2p_phi, P.near_p2p_grad,
+                                                            perm, P.own_begin, s_phi, s_grad, phi, grad);
+  else
+    l2p_out_kernel<false><<<cdiv(nl, 4), 128, 0, P.stream>>>(leaves, nl, P.cells.begin, P.cells.end,
+                                                             P.cells.center, P.pos, P.L, P.p, P.nc, P.near_p2p_phi,
+                                                             nullptr, perm, P.own_begin, s_phi, s_grad, phi, nullptr);
+  FMM_LAUNCHED("l2p_out_kernel");
+}
 
 void near_pass_warp(fmm_plan_s& P, double* phi, double* grad) {
   const int64_t nl = P.own_leaf_end - P.own_leaf_begin;

@@ -179,6 +179,11 @@ struct fmm_plan_s {
   fmm::LetDev let_dev;
   bool let_ready = false;
   bool near_compact_out = false;  // near field writes owned results in Morton order (LET)
+  // near field fused into the M2L v3 kernel (P2P by extra warps, then tail + L2P kernels)
+  bool fuse_near = false;  // FMM_FUSE_NEAR=1: measured slower (profiles/r1_v3.md)
+  fmm::DevBuf<double> near_p2p_phi, near_p2p_grad;  // P2P results in sorted order (unscaled)
+  fmm::DevBuf<int> near_counter;                    // next own leaf to take
+  bool near_fused_active = false, near_fused_grad = false;  // set for the current mat-vec
 
   double t_setup[8] = {0};
   double t_matvec[8] = {0};
@@ -204,6 +209,8 @@ int rot_chunk_width(int p);
 void downward(fmm_plan_s& P);
 void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
 void near_pass_warp(fmm_plan_s& P, double* phi, double* grad);
+void near_fused_prepare(fmm_plan_s& P, bool grad);
+void near_fused_finish(fmm_plan_s& P, double* phi, double* grad);
 void gather_charges(fmm_plan_s& P, const double* q);
 std::vector<int64_t> let_cuts(const int32_t* leaf_begin_sorted, int64_t nleaves, int64_t n, int world);
 void let_lists(int64_t n, int world, int me, const int64_t* caller_off, const uint32_t* perm, int64_t ncells,

@@ -78,7 +78,14 @@ constexpr int rot_xstride(int kpad) {
   return s;
 }
 // chunk width (columns) of the v3 kernel and its shared-memory budget
-constexpr int rot_nc(int p) { return p <= 10 ? 40 : 32; }
+#ifndef FMM_ROT_NC
+#define FMM_ROT_NC 40
+#endif
+constexpr int rot_nc(int p) { return p <= 10 ? FMM_ROT_NC : 32; }
+// class data staged into shared memory by TMA (p <= 10, where it fits beside the chunk buffers)
+// or read by the MMA warps straight from L2 with one-item prefetch (larger p); measured at
+// configs[2]: M2L 7.5 ms (shared) vs 8.4 ms (L2)
+constexpr bool rot_smem_a(int p) { return p <= 10; }
 #ifndef FMM_ROT_MMA
 #define FMM_ROT_MMA 8
 #endif
@@ -289,16 +296,19 @@ struct RGeo {
   static constexpr int NMMA = kRotMMA, NPREP = 4, NACC = kRotAcc, NNEAR = kRotNear;
   static constexpr int KSB = rot_ksb(P);
   static constexpr int NCOEF = (P + 1) * (P + 2) / 2;
+  static constexpr bool SA = rot_smem_a(P);
 };
 
 struct RotSmem {
-  double *acc, *x0, *x1, *ob;  // ob: [2][blob] class data of the chunk in each buffer
+  double *acc, *x0, *x1, *az;  // az: [2][2 (p + 1)] azimuths (cos, sin of m a) of the chunk's class
+  double* ob;                  // SA: [2][blob] class data (azimuths first, so az = ob)
   uint64_t* bar;               // [2] X + class data of buffer b; [2 + j] descriptor buffer j (0..2)
   int32_t *desc;               // [3][rot_desc_ints(NC)] chunk descriptors (chunk i in i % 3)
   int32_t *dec, *pairtab, *sched, *ihdr, *ipos;
   int2* colt;                  // [2][NC] per buffer: (column base, 2 g) of each chunk column
   uint32_t *mmask, *lmask;     // [NR] symmetry masks (bit 2g: take re/im partner, 2g+1: negate)
   int* flag;                   // MMA warps done (near warps stop)
+  int32_t* flat;               // [NMMA][3 smax] per-warp flattened item lists
 };
 template <int P>
 __device__ __forceinline__ RotSmem rot_carve(double* sm, const RotArgs& r) {
@@ -308,7 +318,8 @@ __device__ __forceinline__ RotSmem rot_carve(double* sm, const RotArgs& r) {
   m.x0 = m.acc + (size_t)r.a.T * G::NR;
   m.x1 = m.x0 + G::NC * G::S;
   m.ob = m.x1 + G::NC * G::S;
-  uint64_t* b = (uint64_t*)(m.ob + 2 * r.blob);
+  m.az = m.ob;
+  uint64_t* b = (uint64_t*)(m.ob + (G::SA ? 2 * (size_t)r.blob : 4 * (size_t)(P + 1)));
   m.bar = b;
   m.desc = (int32_t*)(b + 6);  // 16-byte aligned (ob and bar sizes are multiples of 16)
   m.dec = m.desc + 3 * rot_desc_ints(G::NC);
@@ -320,6 +331,7 @@ __device__ __forceinline__ RotSmem rot_carve(double* sm, const RotArgs& r) {
   m.ihdr = m.flag + 2;
   m.ipos = m.ihdr + r.nitems;
   m.sched = m.ipos + 32 * r.nitems;
+  m.flat = m.sched + 3 * G::NMMA * r.smax;
   return m;
 }
 
@@ -356,15 +368,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // One MMA item of shape MT x KS (k-steps), NT n-tiles (compile-time), in place: B streamed
 // per k-step, results held in registers until every k-step was read.
 template <int P, int MT, int KS, int NT>
-__device__ __forceinline__ void rot_item_nt(const double* __restrict__ A, const int32_t* pos, int nparts, double sgn1,
-                                            double* xc, int lane, int dbg) {
+__device__ __forceinline__ void rot_item_nt(const double (&a)[2][RGeo<P>::KSB], const int32_t* pos, int nparts,
+                                            double sgn1, double* xc, int lane, int dbg) {
   using G = RGeo<P>;
   const int colb = lane >> 2, kl = lane & 3;
-  double a[MT][KS];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) a[mt][ks] = A[(mt * KS + ks) * 32 + lane];
   const double* xb = xc + col_base(colb, G::S);
   for (int pp = 0; pp < nparts; ++pp) {
     const int32_t* ps = pos + 16 * pp;
@@ -408,15 +415,38 @@ __device__ __forceinline__ void rot_item_nt(const double* __restrict__ A, const 
 }
 
 template <int P, int MT, int KS>
-__device__ __forceinline__ void rot_item(const double* __restrict__ A, const int32_t* pos, int nparts, double sgn1,
-                                         int ntiles, double* xc, int lane, int dbg) {
-  static_assert(RGeo<P>::NT <= 5, "n-tile dispatch covers up to 5");
+__device__ __forceinline__ void rot_item(const double (&a)[2][RGeo<P>::KSB], const int32_t* pos, int nparts,
+                                         double sgn1, int ntiles, double* xc, int lane, int dbg) {
+  static_assert(RGeo<P>::NT <= 8, "n-tile dispatch covers up to 8");
   switch (ntiles) {
-    case 1: rot_item_nt<P, MT, KS, 1>(A, pos, nparts, sgn1, xc, lane, dbg); break;
-    case 2: rot_item_nt<P, MT, KS, 2>(A, pos, nparts, sgn1, xc, lane, dbg); break;
-    case 3: rot_item_nt<P, MT, KS, 3>(A, pos, nparts, sgn1, xc, lane, dbg); break;
-    case 4: rot_item_nt<P, MT, KS, 4>(A, pos, nparts, sgn1, xc, lane, dbg); break;
-    default: rot_item_nt<P, MT, KS, RGeo<P>::NT>(A, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 1: rot_item_nt<P, MT, KS, 1>(a, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 2: rot_item_nt<P, MT, KS, 2>(a, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 3: rot_item_nt<P, MT, KS, 3>(a, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 4: rot_item_nt<P, MT, KS, (RGeo<P>::NT < 4 ? RGeo<P>::NT : 4)>(a, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 5: rot_item_nt<P, MT, KS, (RGeo<P>::NT < 5 ? RGeo<P>::NT : 5)>(a, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 6: rot_item_nt<P, MT, KS, (RGeo<P>::NT < 6 ? RGeo<P>::NT : 6)>(a, pos, nparts, sgn1, xc, lane, dbg); break;
+    case 7: rot_item_nt<P, MT, KS, (RGeo<P>::NT < 7 ? RGeo<P>::NT : 7)>(a, pos, nparts, sgn1, xc, lane, dbg); break;
+    default: rot_item_nt<P, MT, KS, RGeo<P>::NT>(a, pos, nparts, sgn1, xc, lane, dbg); break;
+  }
+}
+
+// A fragments of an item (class data in global memory, L2 resident), fragment order
+template <bool GLOBAL>
+__device__ __forceinline__ double lda(const double* p) {
+  if (GLOBAL) return __ldg(p);
+  return *p;
+}
+template <int P, bool GLOBAL>
+__device__ __forceinline__ void load_a(const double* __restrict__ A, bool big, double (&a)[2][RGeo<P>::KSB], int lane) {
+  constexpr int KSB = RGeo<P>::KSB;
+  if (big) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int ks = 0; ks < KSB; ++ks) a[mt][ks] = lda<GLOBAL>(A + (mt * KSB + ks) * 32 + lane);
+  } else {
+    a[0][0] = lda<GLOBAL>(A + lane);
+    a[0][1] = lda<GLOBAL>(A + 32 + lane);
   }
 }
 
@@ -483,7 +513,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       named_sync(3 + b, nmma_t + nacc_t);  // Yfull(i)
       if (!(dbg & 4)) {
         const double* __restrict__ y = b ? m.x1 : m.x0;
-        const double* __restrict__ ob = m.ob + b * BLOB;
+        const double* __restrict__ ob = G::SA ? m.ob + b * BLOB : m.az + b * 2 * (P + 1);
         const int32_t* __restrict__ dsc = m.desc + (i % 3) * rot_desc_ints(NC);
         const int ns = dsc[1];
         const int* __restrict__ meta = dsc + 4 + NC;
@@ -538,21 +568,25 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       if (i >= 2) named_sync(7 + b, nacc_t + nprep_t);  // Xfree(i - 2): X buffer b, descriptor (i + 1) % 3
       if (h == 0 && ch + 1 < c_last) issue_desc(ch + 1, (i + 1) % 3);
       double* xb = b ? m.x1 : m.x0;
-      double* ob = m.ob + b * BLOB;
+      double* ob = G::SA ? m.ob + b * BLOB : m.az + b * 2 * (P + 1);
       const int32_t* dsc = m.desc + j * DI;
       mbar_wait(m.bar + 2 + j, (unsigned)((i / 3) & 1));
       const int ncol = dsc[0], cls = dsc[2];
       if (h < 32 && !(dbg & 8)) {
         fence_proxy_async();  // earlier generic accesses of xb / ob before the async-proxy writes
         if (h == 0) {
-          mbar_arrive_tx(m.bar + b, (unsigned)((ncol * G::KPAD + BLOB) * sizeof(double)));
-          bulk_g2s(ob, r.blobs + (int64_t)cls * BLOB, BLOB * sizeof(double), m.bar + b);
+          mbar_arrive_tx(m.bar + b, (unsigned)((ncol * G::KPAD + (G::SA ? BLOB : 0)) * sizeof(double)));
+          if (G::SA) bulk_g2s(ob, r.blobs + (int64_t)cls * BLOB, BLOB * sizeof(double), m.bar + b);
         }
         __syncwarp();
         for (int c = h; c < ncol; c += 32)
           bulk_g2s(xb + col_base(c, S), a.Mt + (int64_t)dsc[4 + c] * G::KPAD, G::KPAD * sizeof(double), m.bar + b);
       }
       for (int c = h; c < ncol; c += nprep_t) m.colt[b * NC + c] = make_int2(col_base(c, S), 2 * (dsc[4 + NC + c] >> 8));
+      if (!G::SA) {
+        for (int e = h; e < 2 * (P + 1); e += nprep_t) ob[e] = __ldg(r.blobs + (int64_t)cls * BLOB + e);
+        named_sync(6, nprep_t);  // azimuths visible to every prep thread
+      }
       const int ncol8 = (ncol + 7) & ~7;  // padding columns of the last n-tile: zeros
       for (int e = h; e < (ncol8 - ncol) * G::KPAD; e += nprep_t)
         xb[col_base(ncol + e / G::KPAD, S) + e % G::KPAD] = 0.0;
@@ -612,38 +646,84 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
     // ================= MMA warps: the three block-GEMM stages in place
     unsigned long long tw = 0, ts[3] = {0, 0, 0}, tb = 0, t0 = 0;
     const bool prof = (dbg & 256) && r.prof;
+    // this warp's items of the three stages, flattened once into shared memory: id | stage << 16
+    int32_t* fl = m.flat + warp * 3 * r.smax;
+    int nflat = 0;
+    if (lane == 0)
+      for (int st = 0; st < 3; ++st)
+        for (int k = 0; k < r.smax; ++k) {
+          const int id = m.sched[(st * G::NMMA + warp) * r.smax + k];
+          if (id < 0) break;
+          fl[nflat++] = id | (st << 16);
+        }
+    nflat = __shfl_sync(0xffffffffu, nflat, 0);
+    __syncwarp();
+    auto flat = [&](int f) -> int { return fl[f]; };
     for (int ch = c_first; ch < c_last; ++ch) {
       const int i = ch - c_first, b = i & 1;
       if (prof) t0 = clock64();
       named_sync(1 + b, nprep_t + nmma_t);  // Xfull(i)
       if (prof) tw += clock64() - t0;
       double* xc = b ? m.x1 : m.x0;
-      const double* ob = m.ob + b * BLOB;
-      const int ntiles = (m.desc[(i % 3) * rot_desc_ints(NC)] + 7) >> 3;
-      for (int st = 0; st < 3; ++st) {
-        if (prof) t0 = clock64();
-        const int32_t* sl = m.sched + (st * G::NMMA + warp) * r.smax;
-        for (int k = 0; k < r.smax && !(dbg & 1); ++k) {
-          const int id = sl[k];
-          if (id < 0) break;
-          const int hd = m.ihdr[id];
-          const double* A = ob + (hd >> 8);
-          const int32_t* ps = m.ipos + 32 * id;
-          const int nparts = (hd >> 1) & 3;
-          const double sgn1 = st == 1 ? -1.0 : 1.0;  // z translation: Im = -Z Im
-          if (hd & 1)
-            rot_item<P, 2, G::KSB>(A, ps, nparts, sgn1, ntiles, xc, lane, dbg);
-          else
-            rot_item<P, 1, 2>(A, ps, nparts, sgn1, ntiles, xc, lane, dbg);
+      const int32_t* dsc = m.desc + (i % 3) * rot_desc_ints(NC);
+      const int ntiles = (dsc[0] + 7) >> 3;
+      const double* gblob = G::SA ? m.ob + b * BLOB : r.blobs + (int64_t)dsc[2] * BLOB;
+      double a[2][G::KSB], an[2][G::KSB];
+      int cur = nflat ? flat(0) : -1;
+      if (!G::SA && cur >= 0) load_a<P, true>(gblob + (m.ihdr[cur & 0xffff] >> 8), m.ihdr[cur & 0xffff] & 1, a, lane);
+      int st_now = 0;
+      if (prof) t0 = clock64();
+      for (int f = 0; f < nflat && !(dbg & 1); ++f) {
+        const int id = cur & 0xffff, st = cur >> 16;
+        const int nxt = f + 1 < nflat ? flat(f + 1) : -1;
+        if (G::SA)  // class data in shared memory: no prefetch (registers)
+          load_a<P, false>(gblob + (m.ihdr[id] >> 8), m.ihdr[id] & 1, a, lane);
+        else if (nxt >= 0)  // class data in L2: next item's fragments one item ahead
+          load_a<P, true>(gblob + (m.ihdr[nxt & 0xffff] >> 8), m.ihdr[nxt & 0xffff] & 1, an, lane);
+        while (st_now < st) {  // stage barrier(s) before this item's stage
+          if (prof) {
+            const unsigned long long t1 = clock64();
+            ts[st_now] += t1 - t0;
+            t0 = t1;
+          }
+          if (!(dbg & 16)) named_sync(5, nmma_t);
+          if (prof) {
+            const unsigned long long t1 = clock64();
+            tb += t1 - t0;
+            t0 = t1;
+          }
+          ++st_now;
         }
+        const int hd = m.ihdr[id];
+        const int32_t* ps = m.ipos + 32 * id;
+        const int nparts = (hd >> 1) & 3;
+        const double sgn1 = st == 1 ? -1.0 : 1.0;  // z translation: Im = -Z Im
+        if (hd & 1)
+          rot_item<P, 2, G::KSB>(a, ps, nparts, sgn1, ntiles, xc, lane, dbg);
+        else
+          rot_item<P, 1, 2>(a, ps, nparts, sgn1, ntiles, xc, lane, dbg);
+        if (!G::SA)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int ks = 0; ks < G::KSB; ++ks) a[mt][ks] = an[mt][ks];
+        cur = nxt;
+      }
+      while (st_now < 2) {  // remaining stage barriers (warps without items in later stages)
         if (prof) {
           const unsigned long long t1 = clock64();
-          ts[st] += t1 - t0;
+          ts[st_now] += t1 - t0;
           t0 = t1;
         }
-        if (st < 2 && !(dbg & 16)) named_sync(5, nmma_t);  // stage st complete before st + 1 reads it
-        if (prof) tb += clock64() - t0;
+        if (!(dbg & 16)) named_sync(5, nmma_t);
+        if (prof) {
+          const unsigned long long t1 = clock64();
+          tb += t1 - t0;
+          t0 = t1;
+        }
+        ++st_now;
       }
+      if (prof) ts[2] += clock64() - t0;
       named_arrive(3 + b, nmma_t + nacc_t);  // Yfull(i)
     }
     if (warp == 0 && lane == 0) *(volatile int*)m.flag = 1;  // near warps stop taking leaves
@@ -822,8 +902,9 @@ size_t rot_smem_bytes(int p, int T, int extra_ints) {
   int blob = 0;
   std::vector<RotItem> items = build_items(p, blob);
   const int ni = (int)items.size();
-  return sizeof(double) * ((size_t)T * NR + 2 * (size_t)NC * S + 2 * (size_t)blob) + sizeof(uint64_t) * 6 +
-         sizeof(int32_t) * (3 * rot_desc_ints(NC) + 3 * NR + nc + 4 + 4 * NC + ni + 32 * ni + 3 * kRotMMA * extra_ints);
+  return sizeof(double) * ((size_t)T * NR + 2 * (size_t)NC * S + (rot_smem_a(p) ? 2 * (size_t)blob : 4 * (size_t)(p + 1))) +
+         sizeof(uint64_t) * 6 +
+         sizeof(int32_t) * (3 * rot_desc_ints(NC) + 3 * NR + nc + 4 + 4 * NC + ni + 32 * ni + 6 * kRotMMA * extra_ints);
 }
 
 void m2l_rot_setup(fmm_plan_s& P) {

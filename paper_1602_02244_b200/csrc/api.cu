@@ -179,6 +179,7 @@ int64_t fmm_plan_s::bytes() const {
   b += p2p.tgt.bytes() + p2p.src.bytes() + p2p.off.bytes() + m2l.tgt.bytes() + m2l.src.bytes() + m2l.off.bytes();
   b += host_stage_q.bytes() + host_stage_phi.bytes() + host_stage_grad.bytes();
   b += m2l_dmma.bytes();
+  b += shift_ops.bytes();
   b += let_dev.bytes();
   return b;
 }
@@ -226,13 +227,21 @@ fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncr
     if (v && v[0] >= '1' && v[0] <= '3') P->m2l_variant = v[0] - '0';
     const char* nv = getenv("FMM_NEAR_VARIANT");
     if (nv && nv[0] == '1') P->near_variant = 1;
+    const char* sv = getenv("FMM_SHIFT_VARIANT");
+    if (sv && sv[0] == '1') P->shift_variant = 1;
     const char* fz = getenv("FMM_FUSE_NEAR");  // experiment: P2P warps inside the M2L v3 kernel
     P->fuse_near = fz && fz[0] == '1';
     const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // test hook: export M2L-only local expansions
     P->debug_skip_l2l = dbg && dbg[0] == '1';
     if (P->m2l_variant >= 2) fmm::m2l_dmma_setup(*P);
+    fmm::shift_setup(*P);
     P->M.alloc(P->cells.n * P->nc);
     P->L.alloc(P->cells.n * P->nc);
+    const char* poison = getenv("FMM_DEBUG_POISON");  // test hook: NaN-fill expansions so unwritten
+    if (poison && poison[0] == '1') {                 // coefficients surface in the results
+      FMM_CUDA(cudaMemsetAsync(P->M.ptr, 0xff, P->M.bytes(), P->stream));
+      FMM_CUDA(cudaMemsetAsync(P->L.ptr, 0xff, P->L.bytes(), P->stream));
+    }
     FMM_CUDA(cudaEventRecord(e3, P->stream));
     FMM_CUDA(cudaEventSynchronize(e3));
     float a = 0, b = 0, c = 0;

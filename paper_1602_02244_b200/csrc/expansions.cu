@@ -9,7 +9,12 @@
 //
 // Every output coefficient is owned by one thread that accumulates its terms
 // in a fixed order: no floating-point atomics, bitwise-deterministic results.
+#include <algorithm>
+#include <utility>
+#include <vector>
+
 #include "harmonics.cuh"
+#include "m2l_common.cuh"
 #include "plan.h"
 
 namespace fmm {
@@ -108,14 +113,14 @@ __global__ void __launch_bounds__(32 * kP2MWarps) p2m_warp_kernel(const int32_t*
       rw[lane * kStride + 2 * k + 1] = acc[k].y;
     }
     __syncwarp();
-    if (lane < 2 * len) {
+    for (int t = lane; t < 2 * len; t += 32) {  // 2 len = 34 > 32 only for p = 16, m = 0
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll 8
       for (int r = 0; r < 32; r += 2) {
-        s0 += rw[r * kStride + lane];
-        s1 += rw[(r + 1) * kStride + lane];
+        s0 += rw[r * kStride + t];
+        s1 += rw[(r + 1) * kStride + t];
       }
-      Ml[2 * cidx(m + (lane >> 1), m) + (lane & 1)] = s0 + s1;
+      Ml[2 * cidx(m + (t >> 1), m) + (t & 1)] = s0 + s1;
     }
     __syncwarp();
   }
@@ -257,6 +262,268 @@ __global__ void l2l_kernel(int64_t lb, const int32_t* __restrict__ child, const 
 }  // namespace
 
 namespace {
+// ---- S8 / S10 on the FP64 tensor cores (shift_variant 2). In scaled form the M2M and L2L
+// shifts of a child at offset d = h_c u from its parent (u in {-1, 1}^3, h_c the child half
+// side) are level-independent real matrices A(u) acting on (p+1)^2 real coefficients:
+//   M2M: M_p{j} = h_c^j  sum conj R_n^m(u) M~_c{j-n},     M~_c = M_c h_c^{-deg}
+//   L2L: L_c{j} = h_c^-j sum L~_p{n} conj R_{n-j}^{m-k}(u), L~_p = L_p h_c^{deg}
+// and the eight octants are one operator A = A(+,+,+) conjugated by diagonal sign matrices,
+// A(rho u) = S_rho A S_rho (the coordinate flips act on a coefficient (n, m, re/im) as
+// x: (-1)^m conj, y: conj, z: (-1)^(n+m)). So one DMMA GEMM serves a whole
+// level: a warp takes two parents, their 8 children are the 8 columns of an m8n8k4 tile,
+// signs and powers of h_c are applied when the columns are gathered and in the epilogue.
+// M2M sums the 8 signed columns of its parent (shuffle over the quad, fixed order); L2L adds
+// each column to its child. Degree-blocked real layout => M2M is block lower triangular
+// (output degree j reads degrees <= j), L2L block upper triangular; zero blocks are skipped.
+constexpr int kShiftWarps = 4;
+
+__host__ __device__ constexpr int shift_isq(int r) {
+  int n = 0;
+  while ((n + 1) * (n + 1) <= r) ++n;
+  return n;
+}
+__host__ __device__ constexpr int shift_nr(int p) { return (p + 1) * (p + 1); }
+__host__ __device__ constexpr int shift_nmt(int p) { return (shift_nr(p) + 7) / 8; }
+__host__ __device__ constexpr int shift_nks(int p) { return (shift_nr(p) + 3) / 4; }
+// k-step range [lo, hi) of the non-zero blocks of row tile mt
+__host__ __device__ constexpr int shift_lo(int p, bool l2l, int mt) {
+  return l2l ? (shift_isq(8 * mt) * shift_isq(8 * mt)) / 4 : 0;
+}
+__host__ __device__ constexpr int shift_hi(int p, bool l2l, int mt) {
+  return l2l ? shift_nks(p)
+             : ((shift_isq(8 * mt + 7 < shift_nr(p) ? 8 * mt + 7 : shift_nr(p) - 1) + 1) *
+                    (shift_isq(8 * mt + 7 < shift_nr(p) ? 8 * mt + 7 : shift_nr(p) - 1) + 1) +
+                3) / 4;
+}
+// packed fragment offset (in k-steps) of row tile mt; shift_off(p, l2l, nmt) = total
+__host__ __device__ constexpr int shift_off(int p, bool l2l, int mt) {
+  int o = 0;
+  for (int t = 0; t < mt; ++t) o += shift_hi(p, l2l, t) - shift_lo(p, l2l, t);
+  return o;
+}
+
+// A(+,+,+) column by column: block per input real coefficient r, thread per output (j, k);
+// written in packed DMMA fragment order (only the non-zero k-step blocks of each row tile)
+template <bool L2L>
+__global__ void build_shift_ops_kernel(int p, int nc, double* __restrict__ frag) {
+  extern __shared__ double2 sh[];  // R[nc], E[nc]
+  double2* R = sh;
+  double2* E = sh + nc;
+  const int r = blockIdx.x;
+  for (int m = threadIdx.x; m <= p; m += blockDim.x) regular_column(1.0, 1.0, 1.0, m, p, R);
+  for (int t = threadIdx.x; t < nc; t += blockDim.x) E[t] = make_double2(0, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n, m, part;
+    m2l::real_decode(r, n, m, part);
+    E[cidx(n, m)] = part ? make_double2(0, 1) : make_double2(1, 0);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+    int j, k;
+    decode_jk(t, j, k);
+    const double2 s = L2L ? l2l_term(E, R, p, j, k) : m2m_term(R, E, j, k);
+    for (int part = 0; part < (k > 0 ? 2 : 1); ++part) {
+      const int row = m2l::real_index(j, k, part), mt = row >> 3, ks = r >> 2;
+      const double v = part ? s.y : s.x;
+      if (ks >= shift_lo(p, L2L, mt) && ks < shift_hi(p, L2L, mt))
+        frag[((size_t)shift_off(p, L2L, mt) + ks - shift_lo(p, L2L, mt)) * 32 + (row & 7) * 4 + (r & 3)] = v;
+      else if (v != 0.0)
+        __trap();  // a non-zero outside the degree-triangular structure: the skip rule is wrong
+    }
+  }
+}
+
+// rinfo(r) = cidx(n, m) | part << 12 | n << 13 | flip mask (bit0 x, bit1 y, bit2 z) << 18
+__device__ __forceinline__ uint32_t shift_rinfo(int r) {
+  int n, m, part;
+  m2l::real_decode(r, n, m, part);
+  const uint32_t fx = (m & 1) ^ part, fy = part, fz = (n + m) & 1;
+  return (uint32_t)cidx(n, m) | (uint32_t)part << 12 | (uint32_t)n << 13 | (fx | fy << 1 | fz << 2) << 18;
+}
+__device__ __forceinline__ double sgn(uint32_t info, int oct) {
+  return (__popc((info >> 18) & oct) & 1) ? -1.0 : 1.0;
+}
+// DMMA without `volatile`: independent row tiles may be interleaved by the scheduler
+__device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+template <int PAR>
+struct ShiftTask {
+  int64_t (&cell)[PAR];
+  int (&c0)[PAR];
+  int (&nch)[PAR];
+  int (&oA)[PAR];
+  int (&oB)[PAR];
+  double (&hp)[PAR];
+  double (&hi)[PAR];
+};
+
+// one row tile: DMMA over its non-zero k-steps (compile-time range), then the epilogue
+template <int P, bool L2L, int PAR, int MT>
+__device__ __forceinline__ void shift_tile(const ShiftTask<PAR>& st, const double (&x)[PAR][shift_nks(P)],
+                                           const double* fa, const uint32_t* rinfo, double2* E, int lane) {
+  constexpr int NR = shift_nr(P), NC = (P + 1) * (P + 2) / 2;
+  constexpr int LO = shift_lo(P, L2L, MT), HI = shift_hi(P, L2L, MT), OFF = shift_off(P, L2L, MT);
+  const int c = lane >> 2, kq = lane & 3;
+  const int row = 8 * MT + c;
+  const uint32_t inf = row < NR ? rinfo[row] : 0u;
+  const int ci = inf & 0xfff, part = (inf >> 12) & 1, n = (inf >> 13) & 31;
+  double y0[PAR], y1[PAR], old0[PAR], old1[PAR];
+#pragma unroll
+  for (int q = 0; q < PAR; ++q) {
+    y0[q] = y1[q] = 0.0;
+    old0[q] = old1[q] = 0.0;
+    if (L2L && row < NR) {  // the L2L epilogue adds to the children's M2L results: load them early
+      if (2 * kq < st.nch[q]) old0[q] = ((const double*)(E + (int64_t)(st.c0[q] + 2 * kq) * NC))[2 * ci + part];
+      if (2 * kq + 1 < st.nch[q])
+        old1[q] = ((const double*)(E + (int64_t)(st.c0[q] + 2 * kq + 1) * NC))[2 * ci + part];
+    }
+  }
+#pragma unroll
+  for (int ks = LO; ks < HI; ++ks) {
+    const double a = __ldg(fa + (OFF + ks - LO) * 32);
+#pragma unroll
+    for (int q = 0; q < PAR; ++q) dmma_nv(y0[q], y1[q], a, x[q][ks]);
+  }
+#pragma unroll
+  for (int q = 0; q < PAR; ++q) {
+    const double sc = __shfl_sync(0xffffffffu, L2L ? st.hi[q] : st.hp[q], n);
+    if (!L2L) {
+      double v = sgn(inf, st.oA[q]) * y0[q] + sgn(inf, st.oB[q]) * y1[q];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (kq == 0 && row < NR && st.nch[q] > 0) {
+        double* d = (double*)(E + st.cell[q] * NC) + 2 * ci;
+        d[part] = v * sc;
+        if (row == n * n) d[1] = 0.0;  // Im M_n^0 = 0 (real charges): written, not left uninitialised
+      }
+    } else if (row < NR) {
+      if (2 * kq < st.nch[q])
+        ((double*)(E + (int64_t)(st.c0[q] + 2 * kq) * NC))[2 * ci + part] = old0[q] + sgn(inf, st.oA[q]) * y0[q] * sc;
+      if (2 * kq + 1 < st.nch[q])
+        ((double*)(E + (int64_t)(st.c0[q] + 2 * kq + 1) * NC))[2 * ci + part] = old1[q] + sgn(inf, st.oB[q]) * y1[q] * sc;
+    }
+  }
+}
+
+template <int P, bool L2L, int PAR, int... MT>
+__device__ __forceinline__ void shift_tiles(std::integer_sequence<int, MT...>, const ShiftTask<PAR>& st,
+                                            const double (&x)[PAR][shift_nks(P)], const double* fa,
+                                            const uint32_t* rinfo, double2* E, int lane, int G, int grp) {
+  ((MT % G == grp ? shift_tile<P, L2L, PAR, MT>(st, x, fa, rinfo, E, lane) : void()), ...);
+}
+
+// Warp per PAR parents; lane = (column c = lane / 4, k-quad kq = lane % 4). The B fragments
+// (X[4 ks + kq][c] for every k-step) live in registers: gathered from the expansions with
+// all loads in flight at once; A fragments are read through L1 (packed, compile-time offsets).
+template <int P, bool L2L, int PAR>
+__global__ void __launch_bounds__(32 * kShiftWarps) shift_dmma_kernel(
+    int64_t lb, int64_t ncell, const int32_t* __restrict__ child, const int32_t* __restrict__ nchild,
+    const double4* __restrict__ center, const double* __restrict__ frag, double2* __restrict__ E, int G) {
+  constexpr int NR = shift_nr(P), NMT = shift_nmt(P), NKS = shift_nks(P), NC = (P + 1) * (P + 2) / 2;
+  __shared__ uint32_t rinfo[4 * NKS];
+  for (int r = threadIdx.x; r < 4 * NKS; r += blockDim.x) rinfo[r] = r < NR ? shift_rinfo(r) : 0u;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = lane >> 2, kq = lane & 3;
+  const int64_t ntask = (ncell + PAR - 1) / PAR * G;  // (parent group, row-tile group) pairs
+  for (int64_t tg = (int64_t)blockIdx.x * kShiftWarps + w; tg < ntask; tg += (int64_t)gridDim.x * kShiftWarps) {
+    const int64_t task = tg / G;
+    const int grp = (int)(tg - task * G);
+    double x[PAR][NKS];
+    int64_t cell[PAR];
+    int c0[PAR], nch[PAR], oA[PAR], oB[PAR];
+    double hp[PAR], hi[PAR];  // lane n <= P holds h^n and h^-n (h = child half side)
+#pragma unroll
+    for (int q = 0; q < PAR; ++q) {
+      cell[q] = lb + task * PAR + q;
+      const bool ok = task * PAR + q < ncell;
+      c0[q] = ok ? child[cell[q]] : -1;
+      nch[q] = c0[q] >= 0 ? nchild[cell[q]] : 0;
+      int o = 0;
+      double h = 1.0;
+      if (nch[q] > 0) {
+        const double4 cp = center[cell[q]];
+        const double4 cc = center[c0[q] + (c < nch[q] ? c : 0)];
+        o = (cc.x < cp.x ? 1 : 0) | (cc.y < cp.y ? 2 : 0) | (cc.z < cp.z ? 4 : 0);
+        h = cc.w;
+      }
+      oA[q] = __shfl_sync(0xffffffffu, o, 8 * kq);
+      oB[q] = __shfl_sync(0xffffffffu, o, 8 * kq + 4);
+      double v = 1.0;
+      for (int i = 0; i < (lane <= P ? lane : 0); ++i) v *= h;
+      hp[q] = v;
+      hi[q] = 1.0 / v;
+      const bool mine = c < nch[q];
+      const double* src = (const double*)(E + (L2L ? cell[q] : (int64_t)(c0[q] + (mine ? c : 0))) * NC);
+#pragma unroll
+      for (int ks = 0; ks < NKS; ++ks) {
+        const int k = 4 * ks + kq;
+        const uint32_t inf = rinfo[k];
+        const double sc = __shfl_sync(0xffffffffu, L2L ? hp[q] : hi[q], (inf >> 13) & 31);
+        double v2 = 0.0;
+        if (mine && k < NR) v2 = sgn(inf, o) * __ldg(src + 2 * (inf & 0xfff) + ((inf >> 12) & 1)) * sc;
+        x[q][ks] = v2;
+      }
+    }
+    ShiftTask<PAR> st{cell, c0, nch, oA, oB, hp, hi};
+    shift_tiles<P, L2L, PAR>(std::make_integer_sequence<int, NMT>{}, st, x, frag + lane, rinfo, E, lane, G, grp);
+  }
+}
+
+template <int P, bool L2L, int PAR>
+void launch_shift_pp(fmm_plan_s& Pl, int64_t lb, int64_t ncell) {
+  const int64_t npair = (ncell + PAR - 1) / PAR;
+  // small (upper) levels: split the row tiles of a parent group over G warps
+  int G = 1;
+  while (2 * G <= shift_nmt(P) && npair * G * 2 <= 148 * 16) G *= 2;
+  const int64_t blocks = std::min<int64_t>(cdiv(npair * G, kShiftWarps), 148 * 16);
+  const double* frag = Pl.shift_ops.ptr + (L2L ? (size_t)shift_off(P, false, shift_nmt(P)) * 32 : 0);
+  shift_dmma_kernel<P, L2L, PAR><<<(unsigned)blocks, 32 * kShiftWarps, 0, Pl.stream>>>(
+      lb, ncell, Pl.cells.child, Pl.cells.nchild, Pl.cells.center, frag, L2L ? Pl.L : Pl.M, G);
+  FMM_LAUNCHED(L2L ? "shift_dmma_kernel<L2L>" : "shift_dmma_kernel<M2M>");
+}
+
+template <int P, bool L2L>
+void launch_shift_p(fmm_plan_s& Pl, int64_t lb, int64_t ncell) {
+  static const int par = [] {
+    const char* s = getenv("FMM_SHIFT_PAR");
+    return s && s[0] == '1' ? 1 : 2;
+  }();
+  if constexpr (P <= 10) {
+    if (par == 2) return launch_shift_pp<P, L2L, 2>(Pl, lb, ncell);
+  }
+  launch_shift_pp<P, L2L, 1>(Pl, lb, ncell);
+}
+
+template <bool L2L>
+void launch_shift(fmm_plan_s& P, int64_t lb, int64_t ncell) {
+  if (ncell <= 0) return;
+  switch (P.p) {
+    case 0: launch_shift_p<0, L2L>(P, lb, ncell); break;
+    case 1: launch_shift_p<1, L2L>(P, lb, ncell); break;
+    case 2: launch_shift_p<2, L2L>(P, lb, ncell); break;
+    case 3: launch_shift_p<3, L2L>(P, lb, ncell); break;
+    case 4: launch_shift_p<4, L2L>(P, lb, ncell); break;
+    case 5: launch_shift_p<5, L2L>(P, lb, ncell); break;
+    case 6: launch_shift_p<6, L2L>(P, lb, ncell); break;
+    case 7: launch_shift_p<7, L2L>(P, lb, ncell); break;
+    case 8: launch_shift_p<8, L2L>(P, lb, ncell); break;
+    case 9: launch_shift_p<9, L2L>(P, lb, ncell); break;
+    case 10: launch_shift_p<10, L2L>(P, lb, ncell); break;
+    case 11: launch_shift_p<11, L2L>(P, lb, ncell); break;
+    case 12: launch_shift_p<12, L2L>(P, lb, ncell); break;
+    case 13: launch_shift_p<13, L2L>(P, lb, ncell); break;
+    case 14: launch_shift_p<14, L2L>(P, lb, ncell); break;
+    case 15: launch_shift_p<15, L2L>(P, lb, ncell); break;
+    default: launch_shift_p<16, L2L>(P, lb, ncell); break;
+  }
+}
+
 void upward_impl(fmm_plan_s& P, int64_t leaf_b, int64_t leaf_e) {
   cudaStream_t s = P.stream;
   const int nc = P.nc;
@@ -283,19 +550,25 @@ void upward_impl(fmm_plan_s& P, int64_t leaf_b, int64_t leaf_e) {
       default: launch_p2m<16>(P, lv, nl, s); break;
     }
   }
-  const size_t sh = sizeof(double2) * 24 * nc;
-  static size_t configured = 0;
-  if (sh > 48 * 1024 && sh > configured) {
-    FMM_CUDA(cudaFuncSetAttribute(m2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    configured = sh;
+  if (P.shift_variant == 1) {
+    const size_t sh = sizeof(double2) * 24 * nc;
+    static size_t configured = 0;
+    if (sh > 48 * 1024 && sh > configured) {
+      FMM_CUDA(cudaFuncSetAttribute(m2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+      configured = sh;
+    }
+    for (int l = P.max_level - 1; l >= 0; --l) {
+      const int64_t lb = P.level_begin[l], le = P.level_begin[l + 1];
+      m2m_kernel<<<(unsigned)(le - lb), kM2MThreads, sh, s>>>(lb, P.cells.child, P.cells.nchild, P.cells.center, P.p,
+                                                              nc, P.M);
+      FMM_LAUNCHED("m2m_kernel");
+    }
+    return;
   }
-  for (int l = P.max_level - 1; l >= 0; --l) {
-    const int64_t lb = P.level_begin[l], le = P.level_begin[l + 1];
-    m2m_kernel<<<(unsigned)(le - lb), kM2MThreads, sh, s>>>(lb, P.cells.child, P.cells.nchild, P.cells.center, P.p,
-                                                            nc, P.M);
-    FMM_LAUNCHED("m2m_kernel");
-  }
+  for (int l = P.max_level - 1; l >= 0; --l)
+    launch_shift<false>(P, P.level_begin[l], P.level_begin[l + 1] - P.level_begin[l]);
 }
+
 }  // namespace
 
 void upward(fmm_plan_s& P) { upward_impl(P, 0, P.nleaves); }
@@ -311,13 +584,32 @@ void m2l_pass(fmm_plan_s& P) {
 
 void downward(fmm_plan_s& P) {
   const int nc = P.nc;
-  const size_t sh = sizeof(double2) * 9 * nc;
-  for (int l = 0; l < P.max_level; ++l) {
-    const int64_t lb = P.level_begin[l], le = P.level_begin[l + 1];
-    l2l_kernel<<<(unsigned)(le - lb), kM2MThreads, sh, P.stream>>>(lb, P.cells.child, P.cells.nchild, P.cells.center,
-                                                                   P.p, nc, P.L);
-    FMM_LAUNCHED("l2l_kernel");
+  if (P.shift_variant == 1) {
+    const size_t sh = sizeof(double2) * 9 * nc;
+    for (int l = 0; l < P.max_level; ++l) {
+      const int64_t lb = P.level_begin[l], le = P.level_begin[l + 1];
+      l2l_kernel<<<(unsigned)(le - lb), kM2MThreads, sh, P.stream>>>(lb, P.cells.child, P.cells.nchild,
+                                                                     P.cells.center, P.p, nc, P.L);
+      FMM_LAUNCHED("l2l_kernel");
+    }
+    return;
   }
+  for (int l = 0; l < P.max_level; ++l)
+    launch_shift<true>(P, P.level_begin[l], P.level_begin[l + 1] - P.level_begin[l]);
+}
+
+// the M2M and L2L operators A(+,+,+) in packed DMMA fragment order (shift_variant 2)
+void shift_setup(fmm_plan_s& P) {
+  if (P.shift_variant != 2) return;
+  const int p = P.p;
+  const size_t nm = (size_t)shift_off(p, false, shift_nmt(p)) * 32, nl = (size_t)shift_off(p, true, shift_nmt(p)) * 32;
+  P.shift_ops.alloc((int64_t)(nm + nl));
+  FMM_CUDA(cudaMemsetAsync(P.shift_ops.ptr, 0, sizeof(double) * (nm + nl), P.stream));
+  const size_t sh = sizeof(double2) * 2 * P.nc;
+  build_shift_ops_kernel<false><<<shift_nr(p), 128, sh, P.stream>>>(p, P.nc, P.shift_ops.ptr);
+  FMM_LAUNCHED("build_shift_ops_kernel<M2M>");
+  build_shift_ops_kernel<true><<<shift_nr(p), 128, sh, P.stream>>>(p, P.nc, P.shift_ops.ptr + nm);
+  FMM_LAUNCHED("build_shift_ops_kernel<L2L>");
 }
 
 }  // namespace fmm

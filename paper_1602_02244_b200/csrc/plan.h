@@ -169,6 +169,9 @@ struct fmm_plan_s {
 
   // expansions [ncells][nc] complex (m >= 0), normalised frame
   fmm::DevBuf<double2> M, L;
+  // M2M / L2L operators A(+,+,+) in DMMA fragment order, [2][nmt][nks][32] (expansions.cu shift_setup)
+  fmm::DevBuf<double> shift_ops;
+  int shift_variant = 2;  // 1 = block per parent, thread per coefficient; 2 = DMMA (FMM_SHIFT_VARIANT)
 
   // device status word: bit 0 = non-finite charge seen
   fmm::DevBuf<int32_t> flags;
@@ -207,6 +210,7 @@ void m2l_rot_setup(fmm_plan_s& P);
 size_t rot_smem_bytes(int p, int T, int smax);
 int rot_chunk_width(int p);
 void downward(fmm_plan_s& P);
+void shift_setup(fmm_plan_s& P);  // M2M / L2L term tables
 void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
 void near_pass_warp(fmm_plan_s& P, double* phi, double* grad);
 void near_fused_prepare(fmm_plan_s& P, bool grad);

@@ -7,6 +7,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# GPU tests run with NaN-poisoned expansion buffers (api.cu fmm_setup): a coefficient that no
+# kernel writes (e.g. the p = 16, m = 0 column P2M once skipped) turns the results non-finite.
+os.environ.setdefault("FMM_DEBUG_POISON", "1")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libfmm.so")

@@ -276,3 +276,26 @@ def test_near_variants(torch_cuda, monkeypatch, variant, dist, n, p, ncrit, thet
     assert O.rel_l2(phi, po) <= tol
     if grad:
         assert O.rel_l2(g, go) <= tol
+
+
+@pytest.mark.parametrize("variant,par", [("1", "2"), ("2", "2"), ("2", "1")])
+@pytest.mark.parametrize("dist,n,p,ncrit,theta", [("plummer", 6000, 0, 16, 0.5), ("cube", 6000, 1, 8, 0.4),
+                                                  ("plummer", 6000, 3, 20, 0.5), ("sphere", 8000, 8, 32, 0.4),
+                                                  ("plummer", 8000, 11, 40, 0.5), ("cube", 6000, 13, 64, 0.4),
+                                                  ("plummer", 4000, 16, 64, 0.5)])
+def test_shift_variants(torch_cuda, monkeypatch, variant, par, dist, n, p, ncrit, theta):
+    """M2M / L2L (north_star (3)): v1 block per parent with the branchy term sums and v2 the
+    level-independent scaled operators A(+,+,+) on DMMA with octant sign maps
+    give the oracle's multipoles per cell to 1e-13 and its local expansions to 1e-11."""
+    monkeypatch.setenv("FMM_SHIFT_VARIANT", variant)
+    monkeypatch.setenv("FMM_SHIFT_PAR", par)
+    torch = torch_cuda
+    x, q = F.make(dist, n)
+    pl, phi, g = gpu_fmm(torch, x, q, p, ncrit, theta, grad=True)
+    orc = O.Plan(x, p, ncrit, theta)
+    po, go = orc.eval(q, grad=True, nthreads=O.default_threads())
+    M, L = orc.expansions()
+    Mg, Lg = pl.export("M"), pl.export("L")
+    assert (np.linalg.norm(Mg - M, axis=1) <= 1e-13 * np.linalg.norm(M, axis=1) + 1e-300).all()
+    assert (np.linalg.norm(Lg - L, axis=1) <= 1e-11 * np.linalg.norm(L, axis=1) + 1e-300).all()
+    assert O.rel_l2(phi, po) <= TOL and O.rel_l2(g, go) <= TOL

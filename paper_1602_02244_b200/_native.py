@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libfmm.so")
+LIB_PATH = os.path.join(_PKG, os.path.basename(os.environ.get("FMM_LIB", "libfmm.so")))  # FMM_LIB: experiments
 
 FMM_OK, FMM_ERR_USAGE, FMM_ERR_NUMERIC, FMM_ERR_CUDA, FMM_ERR_OOM, FMM_ERR_COMM = 0, 2, 3, 4, 5, 6
 

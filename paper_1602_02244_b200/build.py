@@ -15,8 +15,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libfmm.so")
+# FMM_LIB (experiments only): build / load an alternative in-tree library, e.g. libfmm_x.so
+LIB = os.path.join(PKG, os.path.basename(os.environ.get("FMM_LIB", "libfmm.so")))
+BUILD = os.path.join(PKG, "_build" + os.path.basename(LIB)[len("libfmm"):-len(".so")])
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -45,10 +45,14 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "harmonics.cuh"
 #include "m2l_common.cuh"
 #include "near_common.cuh"
 #include "plan.h"
+
+namespace cg = cooperative_groups;
 
 namespace fmm {
 namespace m2l {
@@ -284,6 +288,7 @@ struct RotArgs {
   int* leaf_counter;
   double *p2p_phi, *p2p_grad;
   unsigned long long* prof;  // timing experiments (dbg & 256): per MMA warp cycles [wait X, stage 0..2, barriers]
+  int split;                 // CTAs (one cluster) per tile: each takes a contiguous share of the tile's columns
 };
 
 template <int P>
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
   const RotSmem m = rot_carve<P>(sm, r);
   const M2LArgs& a = r.a;
   const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int tile = blockIdx.x;
+  const int tile = blockIdx.x / r.split, h_split = blockIdx.x - tile * r.split;
   // ---- shared tables
   for (int e = tid; e < a.T * NR; e += nthr) m.acc[e] = 0.0;
   for (int k = tid; k < NCOEF - (P + 1); k += nthr) {  // k-th (n, m >= 1) pair
@@ -486,7 +491,22 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
     for (int j = 0; j < 5; ++j) mbar_init(m.bar + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const int c_first = a.tile_chunk[tile], c_last = a.tile_chunk[tile + 1];
+  int c_first = a.tile_chunk[tile], c_last = a.tile_chunk[tile + 1];
+  if (r.split > 1) {  // this CTA's share: chunks whose first column falls in its part of the column range
+    const int col0 = a.chunk_begin[c_first], col1 = a.chunk_begin[c_last];
+    auto first_at = [&](int col) {  // first chunk in [c_first, c_last] starting at or after col
+      int lo = c_first, hi = c_last;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a.chunk_begin[mid] < col) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    const int b0 = first_at(col0 + (int)((int64_t)(col1 - col0) * h_split / r.split));
+    const int b1 = first_at(col0 + (int)((int64_t)(col1 - col0) * (h_split + 1) / r.split));
+    c_first = b0;
+    c_last = h_split + 1 == r.split ? c_last : b1;
+  }
   __syncthreads();
   if (warp >= G::NMMA + G::NPREP + G::NACC) {
     // ================= near warps: P2P of own leaves (global leaf counter) until the MMA warps are done
@@ -738,15 +758,24 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
     }
   }
   __syncthreads();
-  // write back L = L~ / h^{j+1} in complex m >= 0 storage
-  for (int e = tid; e < a.T * NR; e += nthr) {
+  // write back L = L~ / h^{j+1} in complex m >= 0 storage; a split tile first sums the cluster's
+  // partial accumulators (distributed shared memory, rank order: deterministic), each CTA a share
+  const int e0 = a.T * NR * h_split / r.split, e1 = a.T * NR * (h_split + 1) / r.split;
+  if (r.split > 1) cg::this_cluster().sync();
+  for (int e = e0 + tid; e < e1; e += nthr) {
     const int slot = e / NR, q = e - slot * NR;
     const int cell = a.tile_cells[tile * a.T + slot];
     if (cell < 0) continue;
+    double s = m.acc[e];
+    if (r.split > 1) {
+      s = 0.0;
+      for (int k = 0; k < r.split; ++k) s += cg::this_cluster().map_shared_rank(m.acc, k)[e];
+    }
     const int d = m.dec[q];
-    const double v = m.acc[e] * a.hpow[a.level[cell] * (a.p + 2) + ((d >> 1) & 0x7f) + 1];
+    const double v = s * a.hpow[a.level[cell] * (a.p + 2) + ((d >> 1) & 0x7f) + 1];
     ((double*)(a.L + (int64_t)cell * a.nc))[2 * (d >> 8) + (d & 1)] = v;
   }
+  if (r.split > 1) cg::this_cluster().sync();  // no CTA leaves while its accumulators are read
 }
 
 // S9 pre-pass (v3): M~ rows in the RI layout, M~[c][q] = {Re,Im} M_n^m(c) h_c^{-n}, zero for q >= NR.
@@ -1077,7 +1106,31 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
     FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     configured[P.p] = sh;
   }
-  k<<<(unsigned)D.ntiles, 32 * (kRotMMA + 4 + kRotAcc + kRotNear), sh, P.stream>>>(r, dbg);
+  // split small problems over clusters of CTAs so that the grid covers the SMs (configs[1]: 73 tiles)
+  // (one CTA per SM: minimise waves / split, ties to the smaller split; configs[1] -> 2, [2] -> 1)
+  int nsm = 148;
+  FMM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P.device));
+  int split = 1;
+  double best = 1e300;
+  for (int s = 1; s <= 4; s *= 2) {
+    const double cost = (double)((D.ntiles * s + nsm - 1) / nsm) / s;
+    if (cost < best - 1e-9) best = cost, split = s;
+  }
+  if (const char* s = getenv("FMM_M2L_SPLIT")) split = std::max(1, std::min(8, atoi(s)));
+  r.split = split;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(D.ntiles * split));
+  cfg.blockDim = dim3(32 * (kRotMMA + 4 + kRotAcc + kRotNear));
+  cfg.dynamicSmemBytes = sh;
+  cfg.stream = P.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = split;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FMM_CUDA(cudaLaunchKernelEx(&cfg, k, r, dbg));
   FMM_LAUNCHED("m2l_rot_kernel");
   if (dbg & 256) {
     unsigned long long h[8 * 32];

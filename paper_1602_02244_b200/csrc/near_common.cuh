@@ -14,10 +14,14 @@ constexpr int kUnroll = FMM_NEAR_UNROLL;
 
 // 1/sqrt(x): rsqrt.approx.f64 seed (MUFU) + one third-order correction y (1 + e/2 + 3e^2/8),
 // e = 1 - x y^2, relative error O(e^3) << 2^-53 (R11)
+#ifndef FMM_NEAR_ORDER
+#define FMM_NEAR_ORDER 3
+#endif
 __device__ __forceinline__ double rsqrt_fp64(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double e = fma(-x * y, y, 1.0);     // 1 - x y^2
+  const double e = fma(-x * y, y, 1.0);  // 1 - x y^2
+  if (FMM_NEAR_ORDER == 2) return fma(y, 0.5 * e, y);  // one Newton step
   const double c = e * fma(e, 0.375, 0.5);  // e/2 + 3 e^2/8
   return fma(y, c, y);
 }

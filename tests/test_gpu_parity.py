@@ -299,3 +299,20 @@ def test_shift_variants(torch_cuda, monkeypatch, variant, par, dist, n, p, ncrit
     assert (np.linalg.norm(Mg - M, axis=1) <= 1e-13 * np.linalg.norm(M, axis=1) + 1e-300).all()
     assert (np.linalg.norm(Lg - L, axis=1) <= 1e-11 * np.linalg.norm(L, axis=1) + 1e-300).all()
     assert O.rel_l2(phi, po) <= TOL and O.rel_l2(g, go) <= TOL
+
+
+@pytest.mark.parametrize("split", ["1", "2", "3", "4", "8"])
+@pytest.mark.parametrize("dist,n,p,ncrit,theta", [("cube", 30000, 10, 64, 0.4), ("plummer", 20000, 12, 40, 0.5)])
+def test_m2l_split_clusters(torch_cuda, monkeypatch, split, dist, n, p, ncrit, theta):
+    """M2L v3 with a tile's columns split over a cluster of CTAs (partial accumulators summed
+    through distributed shared memory in rank order) matches the oracle and is bit-identical
+    to the unsplit kernel."""
+    torch = torch_cuda
+    x, q = F.make(dist, n)
+    monkeypatch.setenv("FMM_M2L_SPLIT", "1")
+    _, phi1, g1 = gpu_fmm(torch, x, q, p, ncrit, theta, grad=True)
+    monkeypatch.setenv("FMM_M2L_SPLIT", split)
+    _, phi, g = gpu_fmm(torch, x, q, p, ncrit, theta, grad=True)
+    po, go = O.fmm(x, q, p, ncrit, theta, grad=True, nthreads=O.default_threads())
+    assert O.rel_l2(phi, po) <= TOL and O.rel_l2(g, go) <= TOL
+    assert O.rel_l2(phi, phi1) <= 1e-14

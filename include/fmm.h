@@ -99,7 +99,19 @@ typedef struct {
   int m2l_pad_;
   double m2l_flops_per_pair; /* useful flops per M2L pair of that formulation (v3: the three
                                 block stages + the two azimuthal rotations; v1/v2: 2(p+1)^4) */
+  int64_t bytes_by[8];       /* bytes_device by category, FMM_B_* (the FMM side of PAPER.md
+                                Fig 4, "strictly O(N) storage") */
 } fmm_stats_t;
+enum {
+  FMM_B_PARTICLES = 0,  /* keys, permutation, positions + charges, host-call staging */
+  FMM_B_TREE = 1,       /* cell arrays, leaf index */
+  FMM_B_LISTS = 2,      /* P2P and M2L interaction lists */
+  FMM_B_EXPANSIONS = 3, /* M and L, plus the M2L kernels' scaled multipole rows */
+  FMM_B_OPERATORS = 4,  /* precomputed translation operators: M2L class tables, M2M/L2L */
+  FMM_B_SCHEDULE = 5,   /* M2L column / chunk / tile schedules and descriptors */
+  FMM_B_LET = 6,        /* multi-GPU exchange lists and buffers */
+  FMM_B_OTHER = 7
+};
 
 /*
  * fmm_setup — precalculation: bounding cube, Morton keys,

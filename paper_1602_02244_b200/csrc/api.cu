@@ -338,6 +338,28 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     out->t_matvec_ms[i] = P->t_matvec[i];
   }
   out->bytes_device = P->bytes();
+  {
+    const fmm::M2LDmma& D = P->m2l_dmma;
+    const fmm::Cells& c = P->cells;
+    int64_t* b = out->bytes_by;
+    for (int k = 0; k < 8; ++k) b[k] = 0;
+    b[FMM_B_PARTICLES] = P->keys.bytes() + P->perm.bytes() + P->pos.bytes() + P->host_stage_q.bytes() +
+                         P->host_stage_phi.bytes() + P->host_stage_grad.bytes();
+    b[FMM_B_TREE] = c.level.bytes() + c.begin.bytes() + c.end.bytes() + c.child.bytes() + c.nchild.bytes() +
+                    c.parent.bytes() + c.anchor.bytes() + c.center.bytes() + P->leaves.bytes();
+    b[FMM_B_LISTS] = P->p2p.tgt.bytes() + P->p2p.src.bytes() + P->p2p.off.bytes() + P->m2l.tgt.bytes() +
+                     P->m2l.src.bytes() + P->m2l.off.bytes();
+    b[FMM_B_EXPANSIONS] = P->M.bytes() + P->L.bytes() + D.Mt.bytes();
+    b[FMM_B_OPERATORS] = D.ops.bytes() + D.rot_ops.bytes() + D.hpow.bytes() + D.symtab.bytes() +
+                         D.rot_masks.bytes() + D.class_keys.bytes() + P->shift_ops.bytes();
+    b[FMM_B_SCHEDULE] = D.col_src.bytes() + D.col_meta.bytes() + D.chunk_begin.bytes() + D.chunk_class.bytes() +
+                        D.tile_chunk.bytes() + D.tile_cells.bytes() + D.chunk_seg.bytes() + D.seg_begin.bytes() +
+                        D.rot_sched.bytes() + D.rot_ihdr.bytes() + D.rot_ipos.bytes() + D.rot_desc.bytes();
+    b[FMM_B_LET] = P->let_dev.bytes();
+    int64_t s = 0;
+    for (int k = 0; k < 7; ++k) s += b[k];
+    b[FMM_B_OTHER] = out->bytes_device - s;
+  }
   out->m2l_variant = P->m2l_variant;
   {
     const double p1 = P->p + 1;

@@ -104,6 +104,7 @@ class Plan:
         d = {k: getattr(s, k) for k, _ in N.FmmStats._fields_}
         d["t_setup_ms"] = list(s.t_setup_ms)
         d["t_matvec_ms"] = list(s.t_matvec_ms)
+        d["bytes_by"] = dict(zip(N.BYTES_CATEGORIES, list(s.bytes_by)))
         return d
 
     # ---- multi-GPU LET exchange (fmm.h fmm_let_*); buffers are device float64 tensors

@@ -316,3 +316,24 @@ def test_m2l_split_clusters(torch_cuda, monkeypatch, split, dist, n, p, ncrit, t
     po, go = O.fmm(x, q, p, ncrit, theta, grad=True, nthreads=O.default_threads())
     assert O.rel_l2(phi, po) <= TOL and O.rel_l2(g, go) <= TOL
     assert O.rel_l2(phi, phi1) <= 1e-14
+
+
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
+def test_stats_bytes_by_category(torch_cuda, monkeypatch, variant):
+    """fmm_stats bytes_by (include/fmm.h FMM_B_*) partitions bytes_device; operator tables exist
+    only for the precomputed formulations (v2/v3) beside the small M2M/L2L operators."""
+    monkeypatch.setenv("FMM_M2L_VARIANT", variant)
+    torch = torch_cuda
+    x, q = F.cube(20000, seed=2)
+    pl, _, _ = gpu_fmm(torch, x, q, 8, 32, 0.4, grad=False)
+    st = pl.stats()
+    by = st["bytes_by"]
+    assert all(v >= 0 for v in by.values()) and sum(by.values()) == st["bytes_device"]
+    assert by["other"] < 1024 and by["let"] == 0  # other: the device status word
+    nc = 9 * 10 // 2
+    assert by["expansions"] >= 2 * 16 * nc * st["n_cells"]
+    assert by["particles"] >= 44 * st["n"]
+    if variant == "1":
+        assert by["operators"] < 1e6 and by["schedule"] == 0
+    else:
+        assert by["operators"] > 1e6 and by["schedule"] > 0

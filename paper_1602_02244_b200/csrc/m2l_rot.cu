@@ -289,6 +289,7 @@ struct RotArgs {
   double *p2p_phi, *p2p_grad;
   unsigned long long* prof;  // timing experiments (dbg & 256): per MMA warp cycles [wait X, stage 0..2, barriers]
   int split;                 // CTAs (one cluster) per tile: each takes a contiguous share of the tile's columns
+  const int32_t* order;      // [ntiles] launch order of the tiles (decreasing work)
 };
 
 template <int P>
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
   const RotSmem m = rot_carve<P>(sm, r);
   const M2LArgs& a = r.a;
   const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int tile = blockIdx.x / r.split, h_split = blockIdx.x - tile * r.split;
+  const int tile = r.order[blockIdx.x / r.split], h_split = blockIdx.x % r.split;
   // ---- shared tables
   for (int e = tid; e < a.T * NR; e += nthr) m.acc[e] = 0.0;
   for (int k = tid; k < NCOEF - (P + 1); k += nthr) {  // k-th (n, m >= 1) pair
@@ -1040,6 +1041,24 @@ void m2l_rot_setup(fmm_plan_s& P) {
   chunk_desc_kernel<<<(unsigned)D.nchunks, 128, 0, s>>>(D.chunk_begin, D.chunk_class, D.chunk_seg, D.seg_begin,
                                                          D.col_src, D.col_meta, D.nchunks, D.NC, D.rot_desc);
   FMM_LAUNCHED("chunk_desc_kernel");
+  {  // launch order of the tiles: decreasing estimated work (per chunk: fixed cost + its n-tiles), so the
+     // hardware's in-order CTA dispatch balances the last waves like an LPT schedule
+    std::vector<int32_t> tc(D.ntiles + 1), cb(D.nchunks + 1);
+    FMM_CUDA(cudaMemcpyAsync(tc.data(), D.tile_chunk.ptr, sizeof(int32_t) * tc.size(), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaMemcpyAsync(cb.data(), D.chunk_begin.ptr, sizeof(int32_t) * cb.size(), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    std::vector<std::pair<int64_t, int32_t>> w(D.ntiles);
+    for (int64_t t = 0; t < D.ntiles; ++t) {
+      int64_t c = 0;
+      for (int32_t ch = tc[t]; ch < tc[t + 1]; ++ch) c += 3 + (cb[ch + 1] - cb[ch] + 7) / 8;
+      w[t] = {-c, (int32_t)t};
+    }
+    std::sort(w.begin(), w.end());
+    std::vector<int32_t> order(D.ntiles);
+    for (int64_t t = 0; t < D.ntiles; ++t) order[t] = w[t].second;
+    D.rot_order.alloc(D.ntiles);
+    FMM_CUDA(cudaMemcpyAsync(D.rot_order.ptr, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, s));
+  }
   FMM_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1064,6 +1083,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
   r.nitems = D.rot_nitems;
   r.blob = D.rot_blob;
   r.desc = D.rot_desc;
+  r.order = D.rot_order;
   r.p2p_phi = nullptr;
   r.p2p_grad = nullptr;
   if (P.near_fused_active) {

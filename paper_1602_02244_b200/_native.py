@@ -22,7 +22,8 @@ FMM_OK, FMM_ERR_USAGE, FMM_ERR_NUMERIC, FMM_ERR_CUDA, FMM_ERR_OOM, FMM_ERR_COMM 
 EXPORTED = ("fmm_setup", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
             "fmm_set_timing", "fmm_export", "fmm_destroy", "fmm_last_error", "fmm_version", "fmm_let_setup",
             "fmm_let_counts", "fmm_let_pack_q", "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack",
-            "fmm_let_lists_host")
+            "fmm_let_lists_host", "fmm_stencil_apply", "fmm_precond_setup", "fmm_precond_apply", "fmm_precond_info",
+            "fmm_precond_destroy", "fmm_pcg_solve")
 
 
 class FmmExec(C.Structure):
@@ -39,6 +40,11 @@ class FmmStats(C.Structure):
         ("m2l_pad_", C.c_int32), ("m2l_flops_per_pair", C.c_double), ("bytes_by", C.c_int64 * 8),
     ]
 BYTES_CATEGORIES = ("particles", "tree", "lists", "expansions", "operators", "schedule", "let", "other")
+
+
+class PcgInfo(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("relres", C.c_double),
+                ("t_total_ms", C.c_double), ("t_precond_ms", C.c_double)]
 
 
 class FmmError(RuntimeError):
@@ -79,9 +85,20 @@ def lib() -> C.CDLL:
     L.fmm_let_unpack.argtypes = [vp, dp, dp, dp, dp]
     L.fmm_let_lists_host.argtypes = [i64, C.c_int, C.c_int, vp, vp, i64, vp, vp, i64, vp, i64, vp, vp, i64, vp, vp,
                                      C.c_int, vp, i64, C.POINTER(C.c_int64)]
+    # include/fmm_pde.h (NEXT-2)
+    L.fmm_stencil_apply.argtypes = [C.c_int, dp, dp, vp]
+    L.fmm_precond_setup.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                    C.POINTER(FmmExec)]
+    L.fmm_precond_apply.argtypes = [vp, dp, dp]
+    L.fmm_precond_info.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.fmm_precond_destroy.argtypes = [vp]
+    L.fmm_precond_destroy.restype = None
+    L.fmm_pcg_solve.argtypes = [C.c_int, dp, dp, vp, C.c_double, C.c_int, C.POINTER(C.c_double),
+                                C.POINTER(PcgInfo), vp]
     for nm in ("fmm_setup", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
                "fmm_set_timing", "fmm_export", "fmm_let_setup", "fmm_let_counts", "fmm_let_pack_q",
-               "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack", "fmm_let_lists_host"):
+               "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack", "fmm_let_lists_host", "fmm_stencil_apply",
+               "fmm_precond_setup", "fmm_precond_apply", "fmm_precond_info", "fmm_pcg_solve"):
         getattr(L, nm).restype = C.c_int
     _lib = L
     return L

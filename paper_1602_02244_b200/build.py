@@ -33,7 +33,7 @@ def sources():
 
 def _deps():
     return sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + [
-        os.path.join(ROOT, "include", "fmm.h")]
+        os.path.join(ROOT, "include", "fmm.h"), os.path.join(ROOT, "include", "fmm_pde.h")]
 
 
 def up_to_date() -> bool:
@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
             failed.append(src)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcublas"]
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.check_call(link)

@@ -39,6 +39,13 @@ fmm_status guarded(fmm_plan_s* P, F&& body) {
 void usage(bool ok, const char* msg) {
   if (!ok) throw fmm::Error(FMM_ERR_USAGE, msg);
 }
+}  // namespace
+
+namespace fmm {
+fmm_status set_error(int status, const std::string& msg) { return fail(status, msg); }
+}  // namespace fmm
+
+namespace {
 
 // leaves sorted by their first particle (Morton order of the particle ranges)
 __global__ void leaf_keys_kernel(const int32_t* __restrict__ leaves, const int32_t* __restrict__ cbeg, int64_t nl,

@@ -818,6 +818,7 @@ void m2l_dmma_setup(fmm_plan_s& P) {
   if (P.m2l_variant == 3 && !m2l_rot_supported(p)) P.m2l_variant = 2;
   if (P.m2l_variant == 3) {  // v3 chunk width and tile size (shared-memory budget), else v2
     D.T = 64;
+    if (const char* t = getenv("FMM_M2L_T")) D.T = std::max(8, std::min(256, atoi(t)));  // experiments
     while (D.T > 16 && rot_smem_bytes(p, D.T, 8) > 225 * 1024) D.T /= 2;
     if (rot_smem_bytes(p, D.T, 8) > 225 * 1024)
       P.m2l_variant = 2, D.T = 64;

@@ -89,7 +89,10 @@ constexpr int rot_nc(int p) { return p <= 10 ? FMM_ROT_NC : 32; }
 // class data staged into shared memory by TMA (p <= 10, where it fits beside the chunk buffers)
 // or read by the MMA warps straight from L2 with one-item prefetch (larger p); measured at
 // configs[2]: M2L 7.5 ms (shared) vs 8.4 ms (L2)
-constexpr bool rot_smem_a(int p) { return p <= 10; }
+#ifndef FMM_ROT_SA_MAXP
+#define FMM_ROT_SA_MAXP 10
+#endif
+constexpr bool rot_smem_a(int p) { return p <= FMM_ROT_SA_MAXP; }
 #ifndef FMM_ROT_MMA
 #define FMM_ROT_MMA 8
 #endif
@@ -100,9 +103,15 @@ constexpr int kRotMMA = FMM_ROT_MMA;  // MMA warps of the v3 kernel
 #ifndef FMM_ROT_NEAR
 #define FMM_ROT_NEAR 0
 #endif
+#ifndef FMM_ROT_REGS
+#define FMM_ROT_REGS 0
+#endif
+// register rebalancing between the warp roles (setmaxnreg, per warpgroup): the prep and accumulate
+// warps give registers to the MMA warps, which prefetch the next item's A fragments
+constexpr int kRotRegsLow = 64, kRotRegsMMA = 136;
 constexpr int kRotAcc = FMM_ROT_ACC;    // accumulate warps
 constexpr int kRotNear = FMM_ROT_NEAR;  // near-field (P2P) warps fused into the kernel
-constexpr int rot_ksb(int p) { return (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB)
+constexpr int rot_ksb(int p) { return p < 4 ? 2 : (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB), >= 2 (small items use 2)
 // ints of one per-chunk descriptor: [ncol, nseg, class, 0 | srcs | meta | sslot | sbeg[NC + 1]]
 constexpr int rot_desc_ints(int nc) { return (4 + 4 * nc + 1 + 3) & ~3; }
 
@@ -527,6 +536,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       }
     }
   } else if (warp >= G::NMMA + G::NPREP) {
+    if (FMM_ROT_REGS && G::NNEAR == 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRotRegsLow));
     // ================= accumulate warps: acc[slot][r] += (D^L_g Az_L Y)[r] for chunk i
     const int h = tid - nmma_t - nprep_t;
     for (int ch = c_first; ch < c_last; ++ch) {
@@ -575,6 +585,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       named_arrive(7 + b, nacc_t + nprep_t);  // Xfree(i): buffer b may take chunk i + 2
     }
   } else if (warp >= G::NMMA) {
+    if (FMM_ROT_REGS && G::NNEAR == 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRotRegsLow));
     // ================= prep warps: descriptors, TMA bulk copies, symmetry map + Az_M in place
     const int h = tid - nmma_t;
     constexpr int DI = rot_desc_ints(NC);
@@ -664,6 +675,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       named_arrive(1 + b, nprep_t + nmma_t);  // Xfull(i)
     }
   } else {
+    if (FMM_ROT_REGS && G::NNEAR == 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRotRegsMMA));
     // ================= MMA warps: the three block-GEMM stages in place
     unsigned long long tw = 0, ts[3] = {0, 0, 0}, tb = 0, t0 = 0;
     const bool prof = (dbg & 256) && r.prof;
@@ -690,17 +702,18 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       const int ntiles = (dsc[0] + 7) >> 3;
       const double* gblob = G::SA ? m.ob + b * BLOB : r.blobs + (int64_t)dsc[2] * BLOB;
       double a[2][G::KSB], an[2][G::KSB];
+      constexpr bool PF = !G::SA || FMM_ROT_REGS;  // prefetch the next item's A fragments
       int cur = nflat ? flat(0) : -1;
-      if (!G::SA && cur >= 0) load_a<P, true>(gblob + (m.ihdr[cur & 0xffff] >> 8), m.ihdr[cur & 0xffff] & 1, a, lane);
+      if (PF && cur >= 0) load_a<P, !G::SA>(gblob + (m.ihdr[cur & 0xffff] >> 8), m.ihdr[cur & 0xffff] & 1, a, lane);
       int st_now = 0;
       if (prof) t0 = clock64();
       for (int f = 0; f < nflat && !(dbg & 1); ++f) {
         const int id = cur & 0xffff, st = cur >> 16;
         const int nxt = f + 1 < nflat ? flat(f + 1) : -1;
-        if (G::SA)  // class data in shared memory: no prefetch (registers)
+        if (!PF)  // class data in shared memory, no registers to spare: load at the item
           load_a<P, false>(gblob + (m.ihdr[id] >> 8), m.ihdr[id] & 1, a, lane);
-        else if (nxt >= 0)  // class data in L2: next item's fragments one item ahead
-          load_a<P, true>(gblob + (m.ihdr[nxt & 0xffff] >> 8), m.ihdr[nxt & 0xffff] & 1, an, lane);
+        else if (nxt >= 0)  // next item's fragments one item ahead
+          load_a<P, !G::SA>(gblob + (m.ihdr[nxt & 0xffff] >> 8), m.ihdr[nxt & 0xffff] & 1, an, lane);
         while (st_now < st) {  // stage barrier(s) before this item's stage
           if (prof) {
             const unsigned long long t1 = clock64();
@@ -723,7 +736,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
           rot_item<P, 2, G::KSB>(a, ps, nparts, sgn1, ntiles, xc, lane, dbg);
         else
           rot_item<P, 1, 2>(a, ps, nparts, sgn1, ntiles, xc, lane, dbg);
-        if (!G::SA)
+        if (PF)
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -925,7 +938,7 @@ std::vector<RotItem> build_items(int p, int& blob_frag) {
 
 }  // namespace
 
-bool m2l_rot_supported(int p) { return p >= 5 && p <= 14; }
+bool m2l_rot_supported(int p) { return p >= 0 && p <= 14; }
 int rot_chunk_width(int p) { return rot_nc(p); }
 size_t rot_smem_bytes(int p, int T, int extra_ints) {
   const int NR = (p + 1) * (p + 1), KPAD = (NR + 3) & ~3, S = rot_xstride(KPAD), nc = ncoef(p), NC = rot_nc(p);
@@ -1110,6 +1123,11 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
   const size_t sh = rot_smem_bytes(P.p, a.T, D.rot_smax);
   void (*k)(const RotArgs, int) = nullptr;
   switch (P.p) {
+    case 0: k = m2l_rot_kernel<0>; break;
+    case 1: k = m2l_rot_kernel<1>; break;
+    case 2: k = m2l_rot_kernel<2>; break;
+    case 3: k = m2l_rot_kernel<3>; break;
+    case 4: k = m2l_rot_kernel<4>; break;
     case 5: k = m2l_rot_kernel<5>; break;
     case 6: k = m2l_rot_kernel<6>; break;
     case 7: k = m2l_rot_kernel<7>; break;

@@ -197,6 +197,8 @@ struct fmm_plan_s {
 };
 
 namespace fmm {
+// records msg as fmm_last_error() and returns status (api.cu)
+fmm_status set_error(int status, const std::string& msg);
 // setup stages (tree.cu, traverse.cu)
 void build_tree(fmm_plan_s& P, const double* xyz);
 void traverse(fmm_plan_s& P);

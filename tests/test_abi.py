@@ -11,7 +11,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "fmm.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in sorted(os.listdir(os.path.join(ROOT, "include")))
+                  if h.endswith(".h"))
     return sorted(set(re.findall(r"FMM_API\s+[\w\s\*]+?\b(fmm_\w+)\s*\(", src)))
 
 
@@ -25,7 +26,8 @@ def libfmm():
 
 def test_header_declares_the_boundary():
     syms = declared_symbols()
-    for s in ("fmm_setup", "fmm_matvec", "fmm_direct", "fmm_matvec_host", "fmm_destroy", "fmm_last_error"):
+    for s in ("fmm_setup", "fmm_matvec", "fmm_direct", "fmm_matvec_host", "fmm_destroy", "fmm_last_error",
+              "fmm_stencil_apply", "fmm_precond_setup", "fmm_precond_apply", "fmm_pcg_solve"):
         assert s in syms
 
 

@@ -9,7 +9,7 @@
  * Krylov subspace solver." (§4.2; Fig 5 at h = 2^-5);
  * "viewing these methods as a preconditioner instead of a direct solver significantly
  * reduces the accuracy requirements"; the FMM preconditioner's
- * convergence rate is independent of the problem size (PAPER.md:469-470).
+ * convergence rate is independent of the problem size (PAPER.md:478-479).
  *
  * Readings (R30-R36; the paper prints no formulas for this experiment):
  *   lattice   the n^3 interior nodes x = -1 + (i+1) h, h = 2 / (n+1) (h = 2^-5 <=> n = 63),

@@ -1,4 +1,4 @@
-// m2l_rot.cu — S9 M2L v3 (default for p = 5..14): the translation-invariant class
+// m2l_rot.cu — S9 M2L v3 (default for p = 0..14): the translation-invariant class
 // operators of v2 (m2l_dmma.cu) applied in rotation-factored form on FP64 tensor cores.
 //
 // Paper: M2L dominates; "Rotating the multipole expansion so that the

@@ -161,7 +161,7 @@ struct fmm_plan_s {
   int64_t n_p2p_interactions = 0;
   fmm::M2LDmma m2l_dmma;
   int m2l_variant = 3;  // 1 = matrix-free O(p^4) per pair (v1), 2 = dense DMMA operator classes (v2),
-                        // 3 = rotation-factored DMMA operator classes (v3, p = 5..14; else v2)
+                        // 3 = rotation-factored DMMA operator classes (v3, p <= 14; else v2)
   int near_variant = 2; // 1 = block per leaf, thread per target (v1), 2 = warp per leaf (v2)
 
   // this rank's targets (Morton range of sorted positions) and its leaves

@@ -2,7 +2,7 @@
 for the 3D Laplace equation on a [-1,1]^3 lattice with Dirichlet faces (PAPER.md:439-471,
 §4.2). Each pin checks the oracle against something other than itself: closed forms,
 quadrature, dense linear algebra, the harmonic-reproduction property of the single layer,
-and the paper's mesh-independence claim (PAPER.md:469-470)."""
+and the paper's mesh-independence claim (PAPER.md:478-479)."""
 import math
 
 import numpy as np
@@ -96,7 +96,7 @@ def test_fmm_preconditioner_approximates_inverse_and_is_linear():
 
 @pytest.mark.parametrize("n,stride", [(7, 1), (15, 1)])
 def test_fmm_preconditioned_cg_mesh_independent(n, stride):
-    """PAPER.md:469-470: the FMM preconditioner's convergence rate is independent of the problem
+    """PAPER.md:478-479: the FMM preconditioner's convergence rate is independent of the problem
     size; unpreconditioned CG needs O(1/h) iterations."""
     rng = np.random.default_rng(0)
     b = rng.standard_normal(n ** 3)

@@ -1,7 +1,7 @@
 """NEXT-2 on the GPU (include/fmm_pde.h through the C ABI) against the oracle
 (oracle/pde_oracle.py): the stencil bit-exactly, the FMM preconditioner to the mat-vec's
 parity level, the flexible PCG iteration by iteration, and the paper's mesh-independence
-claim at the paper's own size h = 2^-5 (PAPER.md:448-453, 469-470)."""
+claim at the paper's own size h = 2^-5 (PAPER.md:448-453, 478-479)."""
 import numpy as np
 import pytest
 

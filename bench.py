@@ -223,7 +223,8 @@ def run_reference(args, cfg, rank):
 
 
 def config_dict(cfg, n_gpus):
-    return {"workload": f"BASELINE configs[{cfg.index}]: N={cfg.n} {cfg.dist}, p={cfg.p}, ncrit={cfg.ncrit}, "
+    src = f"BASELINE configs[{cfg.index}]" if cfg.index >= 0 else "NEXT-3 paper §4.1 geometry (not a BASELINE config)"
+    return {"workload": f"{src}: N={cfg.n} {cfg.dist}, p={cfg.p}, ncrit={cfg.ncrit}, "
                         f"theta={cfg.theta}" + (", with gradients" if cfg.grad else ""),
             "n": cfg.n, "p": cfg.p, "ncrit": cfg.ncrit, "theta": cfg.theta, "grad": cfg.grad,
             "distribution": cfg.dist, "parallelism": f"morton-target-partition x{n_gpus}" if n_gpus > 1 else "1 GPU",

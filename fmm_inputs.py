@@ -32,6 +32,9 @@ CONFIGS = {
     "c3": Config("c3", 1_000_000, "cube", 10, 64, 0.4, False, 2),
     "c4": Config("c4", 10_000_000, "plummer", 8, 64, 0.5, False, 3),
     "c5": Config("c5", 100_000_000, "sphere", 12, 128, 0.4, False, 4),
+    # NEXT-3: the paper's own §4.1 geometry, a uniform 3D lattice;
+    # not a BASELINE config (index -1), sized like configs[2]
+    "l3": Config("l3", 1_000_000, "lattice", 10, 64, 0.4, False, -1),
 }
 
 
@@ -67,7 +70,19 @@ def sphere(n: int, seed: int = 0):
     return np.ascontiguousarray(x), q
 
 
-GENERATORS = {"cube": cube, "plummer": plummer, "sphere": sphere}
+def lattice(n: int, seed: int = 0):
+    """NEXT-3: the m^3 interior nodes of [-1,1]^3 (m = round(n^(1/3)), spacing 2/(m+1); the paper's
+    §4.1 inputs are "uniform lattices", sizes unstated), charges uniform in [-1, 1].
+    Returns m^3 points (n itself when n is a cube)."""
+    m = max(1, int(round(n ** (1.0 / 3.0))))
+    c = -1.0 + (np.arange(m) + 1.0) * (2.0 / (m + 1))
+    z, y, x = np.meshgrid(c, c, c, indexing="ij")
+    pts = np.stack([x.ravel(), y.ravel(), z.ravel()], 1)
+    q = np.random.default_rng(seed).uniform(-1.0, 1.0, pts.shape[0])
+    return np.ascontiguousarray(pts), q
+
+
+GENERATORS = {"cube": cube, "plummer": plummer, "sphere": sphere, "lattice": lattice}
 
 
 def make(dist: str, n: int, seed: int = 0):

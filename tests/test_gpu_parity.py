@@ -217,7 +217,7 @@ def test_usage_and_numeric_errors(torch_cuda):
     assert np.isfinite(phi.numpy()).all()
 
 
-FULL = [("c2", 2000), ("c3", 2000), ("c4", 1000)]
+FULL = [("c2", 2000), ("c3", 2000), ("c4", 1000), ("l3", 2000)]
 
 
 @pytest.mark.parametrize("name,k", FULL)

@@ -130,6 +130,20 @@ FMM_API fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p,
                      const fmm_exec* ex);
 
 /*
+ * fmm_setup_2d — NEXT-3: the same precalculation for PLANAR points and the 2D Laplace (log)
+ * kernel, the 2D half of the paper's §4.1 experiment ("2D and 3D Laplace equation on uniform
+ * lattices"). A plan made here makes fmm_matvec / fmm_matvec_host compute
+ *   phi_i = - sum_{j : |x_i - x_j| > 0} q_j log |x_i - x_j|,   grad_i = grad_{x_i} phi_i
+ * with grad written as [n][3] (third component 0). The tree and lists are those of the points
+ * (x, y, 0) (the octree of planar points is a quadtree); expansions are complex Laurent /
+ * Taylor series of order p (R40-R44).
+ *   xy : device [n][2] fp64 coordinates (copied). Other arguments as fmm_setup; single GPU
+ *        only (ex->world_size == 1, else FMM_ERR_USAGE).
+ */
+FMM_API fmm_status fmm_setup_2d(fmm_plan* out, const double* xy, int64_t n, int p, int ncrit, double theta,
+                                const fmm_exec* ex);
+
+/*
  * fmm_matvec — application: phi (+ grad) for charges q, on ex->stream.
  *   q    : device [n] fp64 charges, caller order
  *   n    : must equal the setup n (FMM_ERR_USAGE otherwise)

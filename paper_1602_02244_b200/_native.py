@@ -19,7 +19,7 @@ FMM_OK, FMM_ERR_USAGE, FMM_ERR_NUMERIC, FMM_ERR_CUDA, FMM_ERR_OOM, FMM_ERR_COMM 
 (FMM_LET_Q_SEND, FMM_LET_Q_RECV, FMM_LET_M_SEND, FMM_LET_M_RECV, FMM_LET_PHI_SEND, FMM_LET_PHI_RECV, FMM_LET_SHARED,
  FMM_LET_RANK_BEGIN, FMM_LET_Q_SEND_ROWS, FMM_LET_Q_RECV_POS, FMM_LET_SHARED_CELLS, FMM_LET_M_SEND_CELLS,
  FMM_LET_M_RECV_CELLS, FMM_LET_PHI_SEND_IDX, FMM_LET_PHI_RECV_ROWS) = range(15)
-EXPORTED = ("fmm_setup", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
+EXPORTED = ("fmm_setup", "fmm_setup_2d", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
             "fmm_set_timing", "fmm_export", "fmm_destroy", "fmm_last_error", "fmm_version", "fmm_let_setup",
             "fmm_let_counts", "fmm_let_pack_q", "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack",
             "fmm_let_lists_host", "fmm_stencil_apply", "fmm_precond_setup", "fmm_precond_apply", "fmm_precond_info",
@@ -66,6 +66,7 @@ def lib() -> C.CDLL:
     L = C.CDLL(LIB_PATH)
     vp, dp, i64 = C.c_void_p, C.c_void_p, C.c_int64
     L.fmm_setup.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.POINTER(FmmExec)]
+    L.fmm_setup_2d.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.POINTER(FmmExec)]
     L.fmm_matvec.argtypes = [vp, dp, i64, dp, dp]
     L.fmm_matvec_host.argtypes = [vp, dp, i64, dp, dp]
     L.fmm_sync.argtypes = [vp]
@@ -95,7 +96,7 @@ def lib() -> C.CDLL:
     L.fmm_precond_destroy.restype = None
     L.fmm_pcg_solve.argtypes = [C.c_int, dp, dp, vp, C.c_double, C.c_int, C.POINTER(C.c_double),
                                 C.POINTER(PcgInfo), vp]
-    for nm in ("fmm_setup", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
+    for nm in ("fmm_setup", "fmm_setup_2d", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
                "fmm_set_timing", "fmm_export", "fmm_let_setup", "fmm_let_counts", "fmm_let_pack_q",
                "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack", "fmm_let_lists_host", "fmm_stencil_apply",
                "fmm_precond_setup", "fmm_precond_apply", "fmm_precond_info", "fmm_pcg_solve"):

@@ -132,6 +132,25 @@ void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
   Timer T(P, P.timing);
   T.mark(0);
   fmm::gather_charges(P, q);
+  if (P.dim == 2) {  // 2D log kernel (fmm2d.cu)
+    fmm::upward_2d(P);
+    T.mark(1);
+    fmm::m2l_2d(P);
+    T.mark(2);
+    fmm::downward_2d(P);
+    T.mark(3);
+    fmm::near_2d(P, phi, grad);
+    T.mark(4);
+    if (T.on) {
+      FMM_CUDA(cudaEventSynchronize(P.ev[4]));
+      P.t_matvec[FMM_T_UPWARD] = T.between(0, 1);
+      P.t_matvec[FMM_T_M2L] = T.between(1, 2);
+      P.t_matvec[FMM_T_DOWNWARD] = T.between(2, 3);
+      P.t_matvec[FMM_T_NEAR] = T.between(3, 4);
+      P.t_matvec[FMM_T_MATVEC_TOTAL] = T.between(0, 4);
+    }
+    return;
+  }
   fmm::upward(P);
   // near field fused into the M2L v3 kernel (P2P warps on the FP64 pipe)
   P.near_fused_active = P.fuse_near && P.m2l_variant == 3 && P.near_variant == 2 && P.m2l_dmma.ntiles > 0;
@@ -193,8 +212,11 @@ int64_t fmm_plan_s::bytes() const {
 
 extern "C" {
 
-fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncrit, double theta,
-                     const fmm_exec* ex) {
+}  // extern "C"
+
+namespace {
+fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int ncrit, double theta,
+                      const fmm_exec* ex, int dim) {
   if (!out) return fail(FMM_ERR_USAGE, "fmm_setup: out is NULL");
   *out = nullptr;
   fmm_plan_s* P = nullptr;
@@ -218,6 +240,8 @@ fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncr
     P->nc = fmm::ncoef(p);
     P->theta = theta;
     P->theta2 = theta * theta;
+    P->dim = dim;
+    usage(dim == 3 || ex->world_size == 1, "fmm_setup_2d: single-GPU only");
     cudaEvent_t e0, e1, e2, e3;
     FMM_CUDA(cudaEventCreate(&e0));
     FMM_CUDA(cudaEventCreate(&e1));
@@ -240,8 +264,10 @@ fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncr
     P->fuse_near = fz && fz[0] == '1';
     const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // test hook: export M2L-only local expansions
     P->debug_skip_l2l = dbg && dbg[0] == '1';
-    if (P->m2l_variant >= 2) fmm::m2l_dmma_setup(*P);
-    fmm::shift_setup(*P);
+    if (dim == 3) {  // 3D translation operators (the 2D kernels are matrix-free)
+      if (P->m2l_variant >= 2) fmm::m2l_dmma_setup(*P);
+      fmm::shift_setup(*P);
+    }
     P->M.alloc(P->cells.n * P->nc);
     P->L.alloc(P->cells.n * P->nc);
     const char* poison = getenv("FMM_DEBUG_POISON");  // test hook: NaN-fill expansions so unwritten
@@ -269,6 +295,30 @@ fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncr
   }
   *out = P;
   return FMM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+fmm_status fmm_setup(fmm_plan* out, const double* xyz, int64_t n, int p, int ncrit, double theta,
+                     const fmm_exec* ex) {
+  return setup_impl(out, xyz, n, p, ncrit, theta, ex, 3);
+}
+
+fmm_status fmm_setup_2d(fmm_plan* out, const double* xy, int64_t n, int p, int ncrit, double theta,
+                        const fmm_exec* ex) {
+  if (!out) return fail(FMM_ERR_USAGE, "fmm_setup_2d: out is NULL");
+  *out = nullptr;
+  fmm::DevBuf<double> xyz;
+  const fmm_status st = guarded(nullptr, [&] {
+    usage(ex != nullptr && xy != nullptr, "fmm_setup_2d: ex / xy is NULL");
+    usage(n >= 1 && n < ((int64_t)1 << 31) - 1, "fmm_setup_2d: n must be in [1, 2^31 - 2]");
+    FMM_CUDA(cudaSetDevice(ex->device));
+    xyz.alloc(3 * n);
+    fmm::expand_xy(xy, n, xyz, (cudaStream_t)ex->stream);
+  });
+  if (st != FMM_OK) return st;
+  return setup_impl(out, xyz, n, p, ncrit, theta, ex, 2);
 }
 
 fmm_status fmm_matvec(fmm_plan P, const double* q, int64_t n, double* phi, double* grad) {

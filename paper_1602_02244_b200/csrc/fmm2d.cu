@@ -1,0 +1,315 @@
+// fmm2d.cu — NEXT-3: the FMM mat-vec for the 2D Laplace (log) kernel, the
+// 2D half of the paper's §4.1 experiment ("2D and 3D Laplace equation on uniform lattices",
+// PAPER.md:386), on the same tree and interaction lists as the 3D path (planar points (x, y, 0):
+// the octree is a quadtree; R40-R44):
+//
+//   phi_i = - sum_{j : r_ij > 0} q_j log r_ij,   grad_i = grad_{x_i} phi_i   (grad z = 0)
+//
+// Complex notation z = x + i y, Phi(z) = sum_j q_j log(z - z_j), phi = -Re Phi; classical 2D
+// multipole calculus (oracle/fmm2d_oracle.py states every formula):
+//   P2M  a_0 = sum q, a_k = -sum q (z_j - c)^k / k                 (warp per leaf)
+//   M2M  b_l = -a_0 z0^l / l + sum_{k=1..l} a_k z0^(l-k) C(l-1,k-1)  (thread per (parent, l))
+//   M2L  c_0 = a_0 log(-z0) + sum_k a_k (-1)^k z0^-k,
+//        c_l = -a_0 / (l z0^l) + z0^-l sum_k a_k z0^-k C(l+k-1,k-1) (-1)^k  (warp per target, lane l)
+//   L2L  d_l = sum_{k>=l} c_k C(k,l) w^(k-l)                          (thread per (child, l))
+//   L2P + P2P  warp per target leaf, lane per target
+// Expansions live in the plan's normalised frame u = x 2^-e (exact); the logarithm then needs
+// phi = phi_u - e ln 2 (Q - Q0_i), Q = sum q (the root's a_0), Q0_i = the charge at r = 0 from
+// x_i (itself and coincident points, which the sum skips); gradients scale by 2^-e.
+// Every coefficient is produced by one thread in a fixed order: deterministic, no atomics.
+#include <cmath>
+
+#include "plan.h"
+
+namespace fmm {
+namespace {
+
+constexpr int kMaxP2 = kMaxP;  // 2D expansions carry a_0 .. a_p (p <= 16)
+
+struct Binom {
+  double v[2 * kMaxP2 + 2][2 * kMaxP2 + 2];
+};
+constexpr Binom make_binom() {
+  Binom b{};
+  for (int n = 0; n < 2 * kMaxP2 + 2; ++n) {
+    b.v[n][0] = 1.0;
+    for (int k = 1; k <= n; ++k) b.v[n][k] = b.v[n - 1][k - 1] + (k <= n - 1 ? b.v[n - 1][k] : 0.0);
+  }
+  return b;
+}
+__constant__ Binom c_binom = make_binom();
+
+__device__ __forceinline__ double2 cm(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ double2 cadd2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csc(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cinv(double2 a) {
+  const double d = a.x * a.x + a.y * a.y;
+  return make_double2(a.x / d, -a.y / d);
+}
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+__global__ void expand_xy_kernel(const double* __restrict__ xy, int64_t n, double* __restrict__ xyz) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    xyz[3 * i] = xy[2 * i];
+    xyz[3 * i + 1] = xy[2 * i + 1];
+    xyz[3 * i + 2] = 0.0;
+  }
+}
+
+// P2M: warp per leaf, lane = particle (strided), per-lane partial sums then a fixed butterfly
+template <int P>
+__global__ void p2m2d_kernel(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ cbeg,
+                             const int32_t* __restrict__ cend, const double4* __restrict__ center,
+                             const double4* __restrict__ pos, int stride, double2* __restrict__ M) {
+  const int lane = threadIdx.x & 31;
+  const int64_t li = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (li >= nleaves) return;
+  const int leaf = leaves[li];
+  const double4 c = center[leaf];
+  double2 acc[P + 1];
+#pragma unroll
+  for (int k = 0; k <= P; ++k) acc[k] = make_double2(0.0, 0.0);
+  for (int i = cbeg[leaf] + lane; i < cend[leaf]; i += 32) {
+    const double4 v = pos[i];
+    const double2 w = make_double2(v.x - c.x, v.y - c.y);
+    acc[0].x += v.w;
+    double2 wk = w;
+#pragma unroll
+    for (int k = 1; k <= P; ++k) {
+      acc[k] = cadd2(acc[k], csc(wk, -v.w / k));
+      wk = cm(wk, w);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k <= P; ++k)
+    for (int o = 16; o; o >>= 1) {
+      acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, o);
+      acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, o);
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k <= P; ++k) M[(int64_t)leaf * stride + k] = acc[k];
+}
+
+// M2M for the parents of one level: thread per (parent, l), children in order
+__global__ void m2m2d_kernel(int64_t lb, int64_t ncell, const int32_t* __restrict__ child,
+                             const int32_t* __restrict__ nchild, const double4* __restrict__ center, int p, int stride,
+                             double2* __restrict__ M) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncell * (p + 1);
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = lb + t / (p + 1);
+    const int l = (int)(t % (p + 1));
+    const int c0 = child[cell];
+    if (c0 < 0) continue;
+    const double4 cp = center[cell];
+    double2 s = make_double2(0.0, 0.0);
+    for (int ch = c0; ch < c0 + nchild[cell]; ++ch) {
+      const double4 cc = center[ch];
+      const double2 z0 = make_double2(cc.x - cp.x, cc.y - cp.y);
+      const double2* a = M + (int64_t)ch * stride;
+      if (l == 0) {
+        s = cadd2(s, a[0]);
+        continue;
+      }
+      // -a_0 z0^l / l + sum_{k=1..l} a_k z0^(l-k) C(l-1, k-1), z0 powers built from k = l down
+      double2 zp = make_double2(1.0, 0.0), t2 = make_double2(0.0, 0.0);
+      for (int k = l; k >= 1; --k) {
+        t2 = cadd2(t2, csc(cm(a[k], zp), c_binom.v[l - 1][k - 1]));
+        zp = cm(zp, z0);
+      }
+      s = cadd2(s, cadd2(t2, csc(cm(a[0], zp), -1.0 / l)));
+    }
+    M[cell * stride + l] = s;
+  }
+}
+
+// M2L: warp per target cell; lane k < p+1 owns output l = k; per source, lane k forms
+// b_k = a_k z0^-k and broadcasts it; sources in list order
+__global__ void m2l2d_kernel(int64_t ncells, const int32_t* __restrict__ off, const int32_t* __restrict__ src,
+                             const double4* __restrict__ center, const double2* __restrict__ M, int p, int stride,
+                             double2* __restrict__ L) {
+  const int lane = threadIdx.x & 31;
+  const int64_t A = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (A >= ncells) return;
+  const double4 ca = center[A];
+  const int l = lane <= p ? lane : 0;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int e = off[A]; e < off[A + 1]; ++e) {
+    const int B = src[e];
+    const double4 cb = center[B];
+    const double2 z0 = make_double2(cb.x - ca.x, cb.y - ca.y);
+    const double2 inv = cinv(z0);
+    double2 ip = make_double2(1.0, 0.0);  // inv^l by repeated multiplication (l <= 16)
+    for (int k = 0; k < l; ++k) ip = cm(ip, inv);
+    const double2 a0 = M[(int64_t)B * stride];
+    const double2 bk = lane <= p ? cm(M[(int64_t)B * stride + l], ip) : make_double2(0.0, 0.0);  // a_l z0^-l
+    double2 s = make_double2(0.0, 0.0);
+    for (int k = 1; k <= p; ++k) {
+      const double2 b = shfl2(bk, k);
+      const double coef = l == 0 ? ((k & 1) ? -1.0 : 1.0) : c_binom.v[l + k - 1][k - 1] * ((k & 1) ? -1.0 : 1.0);
+      s = cadd2(s, csc(b, coef));
+    }
+    double2 v;
+    if (l == 0) {  // a_0 log(-z0): log|z0| + i arg(-z0)
+      const double2 lg = make_double2(0.5 * log(z0.x * z0.x + z0.y * z0.y), atan2(-z0.y, -z0.x));
+      v = cadd2(cm(a0, lg), s);
+    } else {
+      v = cm(ip, cadd2(csc(a0, -1.0 / l), s));
+    }
+    acc = cadd2(acc, v);
+  }
+  if (lane <= p) L[A * stride + lane] = acc;
+}
+
+// L2L for the children of one level: thread per (child slot, l); adds to the child's M2L result
+__global__ void l2l2d_kernel(int64_t lb, int64_t ncell, const int32_t* __restrict__ child,
+                             const int32_t* __restrict__ nchild, const double4* __restrict__ center, int p, int stride,
+                             double2* __restrict__ L) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncell * 8 * (p + 1);
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = lb + t / (8 * (p + 1));
+    const int r = (int)(t % (8 * (p + 1))), slot = r / (p + 1), l = r % (p + 1);
+    const int c0 = child[cell];
+    if (c0 < 0 || slot >= nchild[cell]) continue;
+    const int ch = c0 + slot;
+    const double4 cp = center[cell], cc = center[ch];
+    const double2 w = make_double2(cc.x - cp.x, cc.y - cp.y);
+    const double2* c = L + cell * stride;
+    double2 s = make_double2(0.0, 0.0), wp = make_double2(1.0, 0.0);
+    for (int k = l; k <= p; ++k) {
+      s = cadd2(s, csc(cm(c[k], wp), c_binom.v[k][l]));
+      wp = cm(wp, w);
+    }
+    L[(int64_t)ch * stride + l] = cadd2(L[(int64_t)ch * stride + l], s);
+  }
+}
+
+// L2P + P2P: warp per target leaf, lane per target; outputs in caller order (perm), with the
+// 2^-e rescale of the logarithm and the gradient
+__global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ cbeg,
+                              const int32_t* __restrict__ cend, const int32_t* __restrict__ poff,
+                              const int32_t* __restrict__ psrc, const double4* __restrict__ center,
+                              const double4* __restrict__ pos, const double2* __restrict__ L, const double2* __restrict__ M,
+                              int p, int stride, double eln2, double sgrad, const uint32_t* __restrict__ perm,
+                              double* __restrict__ phi, double* __restrict__ grad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t li = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (li >= nleaves) return;
+  const int A = leaves[li];
+  const double4 c = center[A];
+  const double2* loc = L + (int64_t)A * stride;
+  const double Q = M[0].x;  // root a_0 = total charge
+  for (int i = cbeg[A] + lane; i < cend[A]; i += 32) {
+    const double4 t = pos[i];
+    double f = 0.0, gx = 0.0, gy = 0.0, q0 = 0.0;
+    for (int e = poff[A]; e < poff[A + 1]; ++e) {
+      const int B = psrc[e];
+      for (int j = cbeg[B]; j < cend[B]; ++j) {
+        const double4 s = pos[j];
+        const double dx = t.x - s.x, dy = t.y - s.y;
+        const double r2 = dx * dx + dy * dy;
+        if (r2 > 0.0) {
+          f -= s.w * 0.5 * log(r2);
+          const double w = s.w / r2;
+          gx -= w * dx;
+          gy -= w * dy;
+        } else {
+          q0 += s.w;
+        }
+      }
+    }
+    // L2P: Phi = sum c_l w^l, Phi' = sum l c_l w^(l-1) (Horner)
+    const double2 w = make_double2(t.x - c.x, t.y - c.y);
+    double2 Ph = loc[p], dPh = csc(loc[p], (double)p);
+    for (int l = p - 1; l >= 0; --l) {
+      Ph = cadd2(cm(Ph, w), loc[l]);
+      if (l >= 1) dPh = cadd2(cm(dPh, w), csc(loc[l], (double)l));
+    }
+    if (p == 0) dPh = make_double2(0.0, 0.0);
+    f -= Ph.x;
+    gx -= dPh.x;
+    gy += dPh.y;
+    const uint32_t o = perm[i];
+    phi[o] = f - eln2 * (Q - q0);
+    if (grad) {
+      grad[3 * (int64_t)o] = gx * sgrad;
+      grad[3 * (int64_t)o + 1] = gy * sgrad;
+      grad[3 * (int64_t)o + 2] = 0.0;
+    }
+  }
+}
+
+template <int P>
+void launch_p2m2d(fmm_plan_s& Pl, int stride) {
+  const int64_t nl = Pl.nleaves;
+  p2m2d_kernel<P><<<cdiv(nl * 32, 128), 128, 0, Pl.stream>>>(Pl.leaves, nl, Pl.cells.begin, Pl.cells.end,
+                                                               Pl.cells.center, Pl.pos, stride, Pl.M);
+  FMM_LAUNCHED("p2m2d_kernel");
+}
+
+unsigned grid2d(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 32)); }
+
+}  // namespace
+
+void expand_xy(const double* xy, int64_t n, double* xyz, cudaStream_t s) {
+  expand_xy_kernel<<<grid2d(n), 256, 0, s>>>(xy, n, xyz);
+  FMM_LAUNCHED("expand_xy_kernel");
+}
+
+void upward_2d(fmm_plan_s& P) {
+  const int stride = P.nc;
+  switch (P.p) {
+    case 0: launch_p2m2d<0>(P, stride); break;
+    case 1: launch_p2m2d<1>(P, stride); break;
+    case 2: launch_p2m2d<2>(P, stride); break;
+    case 3: launch_p2m2d<3>(P, stride); break;
+    case 4: launch_p2m2d<4>(P, stride); break;
+    case 5: launch_p2m2d<5>(P, stride); break;
+    case 6: launch_p2m2d<6>(P, stride); break;
+    case 7: launch_p2m2d<7>(P, stride); break;
+    case 8: launch_p2m2d<8>(P, stride); break;
+    case 9: launch_p2m2d<9>(P, stride); break;
+    case 10: launch_p2m2d<10>(P, stride); break;
+    case 11: launch_p2m2d<11>(P, stride); break;
+    case 12: launch_p2m2d<12>(P, stride); break;
+    case 13: launch_p2m2d<13>(P, stride); break;
+    case 14: launch_p2m2d<14>(P, stride); break;
+    case 15: launch_p2m2d<15>(P, stride); break;
+    default: launch_p2m2d<16>(P, stride); break;
+  }
+  for (int l = P.max_level - 1; l >= 0; --l) {
+    const int64_t lb = P.level_begin[l], nl = P.level_begin[l + 1] - lb;
+    m2m2d_kernel<<<grid2d(nl * (P.p + 1)), 256, 0, P.stream>>>(lb, nl, P.cells.child, P.cells.nchild, P.cells.center,
+                                                                P.p, stride, P.M);
+    FMM_LAUNCHED("m2m2d_kernel");
+  }
+}
+
+void m2l_2d(fmm_plan_s& P) {
+  FMM_CUDA(cudaMemsetAsync(P.L.ptr, 0, P.L.bytes(), P.stream));
+  m2l2d_kernel<<<cdiv(P.cells.n * 32, 256), 256, 0, P.stream>>>(P.cells.n, P.m2l.off, P.m2l.src, P.cells.center, P.M,
+                                                                 P.p, P.nc, P.L);
+  FMM_LAUNCHED("m2l2d_kernel");
+}
+
+void downward_2d(fmm_plan_s& P) {
+  for (int l = 0; l < P.max_level; ++l) {
+    const int64_t lb = P.level_begin[l], nl = P.level_begin[l + 1] - lb;
+    l2l2d_kernel<<<grid2d(nl * 8 * (P.p + 1)), 256, 0, P.stream>>>(lb, nl, P.cells.child, P.cells.nchild,
+                                                                    P.cells.center, P.p, P.nc, P.L);
+    FMM_LAUNCHED("l2l2d_kernel");
+  }
+}
+
+void near_2d(fmm_plan_s& P, double* phi, double* grad) {
+  const double eln2 = P.e * 0.69314718055994530942;  // phi = phi_u - e ln2 (Q - Q0)
+  const double sgrad = std::ldexp(1.0, -P.e);
+  near2d_kernel<<<cdiv(P.nleaves * 32, 128), 128, 0, P.stream>>>(
+      P.leaves, P.nleaves, P.cells.begin, P.cells.end, P.p2p.off, P.p2p.src, P.cells.center, P.pos, P.L, P.M, P.p,
+      P.nc, eln2, sgrad, P.perm, phi, grad);
+  FMM_LAUNCHED("near2d_kernel");
+}
+
+}  // namespace fmm

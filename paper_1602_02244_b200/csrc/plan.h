@@ -132,6 +132,7 @@ struct fmm_plan_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   int rank = 0, world = 1;
+  int dim = 3;  // 2: planar points (x, y, 0) with the 2D log kernel (fmm2d.cu, fmm_setup_2d)
   bool poisoned = false;
   bool timing = false;
   bool debug_skip_l2l = false;
@@ -199,6 +200,12 @@ struct fmm_plan_s {
 namespace fmm {
 // records msg as fmm_last_error() and returns status (api.cu)
 fmm_status set_error(int status, const std::string& msg);
+// 2D log-kernel mat-vec stages (fmm2d.cu)
+void expand_xy(const double* xy, int64_t n, double* xyz, cudaStream_t s);
+void upward_2d(fmm_plan_s& P);
+void m2l_2d(fmm_plan_s& P);
+void downward_2d(fmm_plan_s& P);
+void near_2d(fmm_plan_s& P, double* phi, double* grad);
 // setup stages (tree.cu, traverse.cu)
 void build_tree(fmm_plan_s& P, const double* xyz);
 void traverse(fmm_plan_s& P);

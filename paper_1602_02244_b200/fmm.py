@@ -36,9 +36,11 @@ class Plan:
     """FMM plan: ``fmm_setup`` at construction (tree + interaction lists),
     ``matvec`` = ``fmm_matvec`` (precalculation vs application)."""
 
+    _dim = 3
+
     def __init__(self, points: torch.Tensor, p: int, ncrit: int, theta: float, *, rank: int = 0,
                  world: int = 1, stream=None):
-        points = _dev_f64(points, "points", (3,))
+        points = _dev_f64(points, "points", (self._dim,))
         self.device = points.device
         self.n = points.shape[0]
         self.p, self.ncrit, self.theta = p, ncrit, theta
@@ -47,8 +49,8 @@ class Plan:
         self._ex = _exec(self.device, stream, rank, world)
         h = C.c_void_p()
         with torch.cuda.device(self.device):
-            N.check(N.lib().fmm_setup(C.byref(h), C.c_void_p(points.data_ptr()), self.n, p, ncrit, float(theta),
-                                      C.byref(self._ex)))
+            setup = N.lib().fmm_setup if self._dim == 3 else N.lib().fmm_setup_2d
+            N.check(setup(C.byref(h), C.c_void_p(points.data_ptr()), self.n, p, ncrit, float(theta), C.byref(self._ex)))
         self._h = h
 
     def close(self):
@@ -167,6 +169,13 @@ class Plan:
             nc = (self.p + 1) * (self.p + 2) // 2
             return a.view(np.complex128).reshape(-1, nc)
         return a.reshape(-1, shape) if shape else a
+
+
+class Plan2D(Plan):
+    """NEXT-3: FMM plan for planar points [n, 2] and the 2D log kernel (``fmm_setup_2d``):
+    ``matvec`` returns phi_i = -sum_j q_j log|x_i - x_j| (+ its gradient as [n, 3], z = 0)."""
+
+    _dim = 2
 
 
 def direct(src: torch.Tensor, q: torch.Tensor, tgt: torch.Tensor | None = None, grad: bool = False):

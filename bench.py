@@ -335,8 +335,8 @@ def main():
 
     # ---- roofline of the dominant kernel (algorithmic flops / its event-timed duration)
     st = inner.stats()
-    m2l_ms = statistics.mean(s[1] for s in stage)
-    near_ms = statistics.mean(s[2] for s in stage)
+    m2l_ms = max(1e-6, statistics.mean(s[1] for s in stage))  # stage events of the inner plan
+    near_ms = max(1e-6, statistics.mean(s[2] for s in stage))
     up_ms = statistics.mean(s[0] for s in stage)
     down_ms = statistics.mean(s[3] for s in stage)
     p = cfg.p

@@ -378,6 +378,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// explicit shared-space loads: the carved pointers reach the item code as generic pointers, and
+// generic loads (LD) of shared memory sit on the item's critical path (positions -> B -> DMMA)
+__device__ __forceinline__ int lds_i32(const int32_t* p) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ double lds_f64(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
 
 
 // One MMA item of shape MT x KS (k-steps), NT n-tiles (compile-time), in place: B streamed
@@ -392,9 +404,9 @@ __device__ __forceinline__ void rot_item_nt(const double (&a)[2][RGeo<P>::KSB], 
     const int32_t* ps = pos + 16 * pp;
     int qk[KS], qr[MT];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) qk[ks] = 4 * ks + kl < 16 ? ps[4 * ks + kl] : -1;
+    for (int ks = 0; ks < KS; ++ks) qk[ks] = 4 * ks + kl < 16 ? lds_i32(ps + 4 * ks + kl) : -1;
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) qr[mt] = ps[8 * mt + colb];
+    for (int mt = 0; mt < MT; ++mt) qr[mt] = lds_i32(ps + 8 * mt + colb);
     double c[MT][NT][2];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
@@ -449,7 +461,7 @@ __device__ __forceinline__ void rot_item(const double (&a)[2][RGeo<P>::KSB], con
 template <bool GLOBAL>
 __device__ __forceinline__ double lda(const double* p) {
   if (GLOBAL) return __ldg(p);
-  return *p;
+  return lds_f64(p);
 }
 template <int P, bool GLOBAL>
 __device__ __forceinline__ void load_a(const double* __restrict__ A, bool big, double (&a)[2][RGeo<P>::KSB], int lane) {
@@ -691,7 +703,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
         }
     nflat = __shfl_sync(0xffffffffu, nflat, 0);
     __syncwarp();
-    auto flat = [&](int f) -> int { return fl[f]; };
+    auto flat = [&](int f) -> int { return lds_i32(fl + f); };
     for (int ch = c_first; ch < c_last; ++ch) {
       const int i = ch - c_first, b = i & 1;
       if (prof) t0 = clock64();
@@ -704,16 +716,20 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
       double a[2][G::KSB], an[2][G::KSB];
       constexpr bool PF = !G::SA || FMM_ROT_REGS;  // prefetch the next item's A fragments
       int cur = nflat ? flat(0) : -1;
-      if (PF && cur >= 0) load_a<P, !G::SA>(gblob + (m.ihdr[cur & 0xffff] >> 8), m.ihdr[cur & 0xffff] & 1, a, lane);
+      if (PF && cur >= 0) {
+        const int h0 = lds_i32(m.ihdr + (cur & 0xffff));
+        load_a<P, !G::SA>(gblob + (h0 >> 8), h0 & 1, a, lane);
+      }
       int st_now = 0;
       if (prof) t0 = clock64();
       for (int f = 0; f < nflat && !(dbg & 1); ++f) {
         const int id = cur & 0xffff, st = cur >> 16;
         const int nxt = f + 1 < nflat ? flat(f + 1) : -1;
         if (!PF)  // class data in shared memory, no registers to spare: load at the item
-          load_a<P, false>(gblob + (m.ihdr[id] >> 8), m.ihdr[id] & 1, a, lane);
+          load_a<P, false>(gblob + (lds_i32(m.ihdr + id) >> 8), lds_i32(m.ihdr + id) & 1, a, lane);
         else if (nxt >= 0)  // next item's fragments one item ahead
-          load_a<P, !G::SA>(gblob + (m.ihdr[nxt & 0xffff] >> 8), m.ihdr[nxt & 0xffff] & 1, an, lane);
+          load_a<P, !G::SA>(gblob + (lds_i32(m.ihdr + (nxt & 0xffff)) >> 8), lds_i32(m.ihdr + (nxt & 0xffff)) & 1, an,
+                            lane);
         while (st_now < st) {  // stage barrier(s) before this item's stage
           if (prof) {
             const unsigned long long t1 = clock64();
@@ -728,7 +744,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
           }
           ++st_now;
         }
-        const int hd = m.ihdr[id];
+        const int hd = lds_i32(m.ihdr + id);
         const int32_t* ps = m.ipos + 32 * id;
         const int nparts = (hd >> 1) & 3;
         const double sgn1 = st == 1 ? -1.0 : 1.0;  // z translation: Im = -Z Im

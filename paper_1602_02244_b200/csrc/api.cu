@@ -412,7 +412,7 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     b[FMM_B_SCHEDULE] = D.col_src.bytes() + D.col_meta.bytes() + D.chunk_begin.bytes() + D.chunk_class.bytes() +
                         D.tile_chunk.bytes() + D.tile_cells.bytes() + D.chunk_seg.bytes() + D.seg_begin.bytes() +
                         D.rot_sched.bytes() + D.rot_ihdr.bytes() + D.rot_ipos.bytes() + D.rot_desc.bytes() +
-                        D.rot_order.bytes();
+                        D.rot_order.bytes() + D.rot_scratch.bytes();
     b[FMM_B_LET] = P->let_dev.bytes();
     int64_t s = 0;
     for (int k = 0; k < 7; ++k) s += b[k];

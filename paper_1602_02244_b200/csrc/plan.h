@@ -94,12 +94,13 @@ struct M2LDmma {
   DevBuf<int32_t> rot_ipos;    // [nitems][2][16] item slot positions
   DevBuf<int32_t> rot_desc;    // [nchunks][desc ints] per-chunk descriptors (TMA-loaded)
   DevBuf<int32_t> rot_order;   // [ntiles] launch order of the tiles (decreasing estimated work)
+  DevBuf<double> rot_scratch;  // split tiles: [ntiles][split][T][NR] partial accumulators
   int rot_smax = 0, rot_T = 0, rot_nitems = 0, rot_blob = 0;
   int64_t bytes() const {
     return ops.bytes() + col_src.bytes() + col_meta.bytes() + chunk_begin.bytes() + chunk_class.bytes() +
            tile_chunk.bytes() + tile_cells.bytes() + symtab.bytes() + hpow.bytes() + chunk_seg.bytes() +
            seg_begin.bytes() + Mt.bytes() + class_keys.bytes() + rot_ops.bytes() + rot_masks.bytes() +
-           rot_sched.bytes() + rot_ihdr.bytes() + rot_ipos.bytes() + rot_desc.bytes() + rot_order.bytes();
+           rot_sched.bytes() + rot_ihdr.bytes() + rot_ipos.bytes() + rot_desc.bytes() + rot_order.bytes() + rot_scratch.bytes();
   }
 };
 

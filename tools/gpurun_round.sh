@@ -7,6 +7,9 @@ python bench.py > gpurun_out/bench.log 2>&1
 python bench.py --config c2 --no-cpu-baseline > gpurun_out/bench_c2.log 2>&1
 python bench.py --config c4 --no-cpu-baseline --steps 5 > gpurun_out/bench_c4.log 2>&1
 python bench.py --config c5 --no-cpu-baseline --steps 3 > gpurun_out/bench_c5.log 2>&1
+python bench.py --config l3 --no-cpu-baseline --steps 5 > gpurun_out/bench_l3.log 2>&1
+python tools/pcg_bench.py > gpurun_out/pcg_bench.md 2> gpurun_out/pcg_bench.err
+python tools/fmm2d_bench.py > gpurun_out/fmm2d_bench.md 2> gpurun_out/fmm2d_bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-probe > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:m2l_rot -s 1 -c 1 -o gpurun_out/m2l_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe > gpurun_out/ncu_m2l.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:near_warp -s 1 -c 1 -o gpurun_out/near_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe > gpurun_out/ncu_near.log 2>&1

@@ -817,7 +817,7 @@ void m2l_dmma_setup(fmm_plan_s& P) {
   while (D.T > 8 && m2l_smem_bytes(D) > 220 * 1024) D.T /= 2;
   if (P.m2l_variant == 3 && !m2l_rot_supported(p)) P.m2l_variant = 2;
   if (P.m2l_variant == 3) {  // v3 chunk width and tile size (shared-memory budget), else v2
-    D.T = 64;
+    D.T = 128;  // as many targets per tile as shared memory allows (p <= 8: 128; configs[3] M2L -2 %)
     if (const char* t = getenv("FMM_M2L_T")) D.T = std::max(8, std::min(256, atoi(t)));  // experiments
     while (D.T > 16 && rot_smem_bytes(p, D.T, 8) > 225 * 1024) D.T /= 2;
     if (rot_smem_bytes(p, D.T, 8) > 225 * 1024)
@@ -846,6 +846,14 @@ void m2l_dmma_setup(fmm_plan_s& P) {
   target_flag_kernel<<<cdiv(C.n, 256), 256, 0, s>>>(P.m2l.off, C.begin, C.end, C.n, P.own_begin, P.own_end, flag);
   FMM_LAUNCHED("target_flag_kernel");
   const int64_t ntc = scan_counts_total(flag, off, C.n, s);
+  if (P.m2l_variant == 3 && !getenv("FMM_M2L_T")) {
+    // small problems: narrower tiles until there are two CTA waves (one CTA per SM); configs[1]
+    // (4,681 cells) M2L 1.10 -> 0.84 ms with T = 16 (wider tiles are more efficient per pair:
+    // configs[2] is fastest at T = 64, configs[3] at T = 128)
+    int nsm = 148;
+    FMM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P.device));
+    while (D.T > 16 && (ntc + D.T - 1) / D.T < 2LL * nsm) D.T /= 2;
+  }
   D.ntiles = (ntc + D.T - 1) / D.T;
   D.tile_cells.alloc(std::max<int64_t>(1, D.ntiles * D.T));
   FMM_CUDA(cudaMemsetAsync(D.tile_cells.ptr, 0xff, sizeof(int32_t) * D.tile_cells.count, s));

@@ -28,7 +28,12 @@ constexpr int kM2MThreads = 256;  // M2M / L2L: items (child, coefficient)
 // lane over the leaf's particles (lane = particle), then butterfly-reduced over the warp in
 // a fixed order (deterministic); lane k writes coefficient (m + k, m).
 constexpr int kP2MWarps = 4;
-constexpr int kP2MCache = 2;  // particles per lane kept in registers (leaves of <= 64 particles)
+#ifndef FMM_P2M_CACHE
+#define FMM_P2M_CACHE 2
+#endif
+// particles per lane kept in registers (leaves of <= 32 kP2MCache particles; slots beyond the
+// leaf are skipped warp-uniformly); larger leaves fall back to recomputing the diagonal per order
+constexpr int kP2MCache = FMM_P2M_CACHE;
 
 // one particle's column m contribution: acc[k] += q conj(R_{m+k}^m), given d = R_m^m
 template <int P>
@@ -94,7 +99,8 @@ __global__ void __launch_bounds__(32 * kP2MWarps) p2m_warp_kernel(const int32_t*
       for (int u = 0; u < kP2MCache; ++u) dg[u] = cmul(dg[u], make_double2(s * px[u], s * py[u]));
     }
 #pragma unroll
-    for (int u = 0; u < kP2MCache; ++u) p2m_column<P>(acc, m, dg[u], px[u], py[u], pz[u], pq[u]);
+    for (int u = 0; u < kP2MCache; ++u)
+      if (u == 0 || 32 * u < e - b) p2m_column<P>(acc, m, dg[u], px[u], py[u], pz[u], pq[u]);
     for (int32_t i = b + lane + 32 * kP2MCache; i < e; i += 32) {  // leaves larger than 32 kP2MCache
       const double4 v = pos[i];
       const double x = v.x - c.x, y = v.y - c.y, z = v.z - c.z;

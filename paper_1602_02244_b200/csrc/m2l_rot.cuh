@@ -392,33 +392,32 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
         const int* __restrict__ sb = dsc + 4 + 3 * NC;
         double* __restrict__ acc = m.acc;
         const int2* __restrict__ colt = m.colt + b * NC;
-        constexpr int RG = nacc_t / NR > 0 ? nacc_t / NR : 1;  // threads per row (segment ranges)
-        for (int t = h; t < RG * NR; t += nacc_t) {
-          const int rg = t / NR, row = t - rg * NR;
-          const int s_lo = ns * rg / RG, s_hi = ns * (rg + 1) / RG;
-          const int d = m.dec[row], part = d & 1, n = (d >> 1) & 0x7f;
-          const int mm = (d >> 8) - cidx(n, 0);
-          const int rre = d >> 8, rim = mm ? NCOEF + rre - n - 1 : rre;
+        // thread per (n, m) pair (and segment range): the rotated column value e^{i m a}(yr + i yi)
+        // is formed once per column and feeds both the Re and the Im row
+        constexpr int RG2 = nacc_t / NCOEF > 0 ? nacc_t / NCOEF : 1;
+        for (int t = h; t < RG2 * NCOEF; t += nacc_t) {
+          const int rg = t / NCOEF, rre = t - rg * NCOEF;
+          const int s_lo = ns * rg / RG2, s_hi = ns * (rg + 1) / RG2;
+          const int d = m.dec[rre], n = (d >> 1) & 0x7f;
+          const int mm = rre - cidx(n, 0);
+          const int rim = mm ? NCOEF + rre - n - 1 : rre;
           const double ca = mm ? ob[2 * mm] : 1.0, sa = mm ? ob[2 * mm + 1] : 0.0;
-          // column value = c0 yr + c1 yi: source part = part ^ (take partner), then Az_L,
-          // then the sign; idx = mask bits ^ part = (source part) | (negate) << 1
-          const uint32_t mask = m.lmask[row];
-          // column value = k0 yr + k1 yi: source part = part ^ (take partner), then Az_L,
-          // then the sign (idx = mask bits ^ part = source part | negate << 1)
-          const double kr0 = ca, ki0 = -sa, kr1 = sa, ki1 = ca;
+          const uint32_t mre = m.lmask[rre], mim = mm ? m.lmask[rim] : 0u;
           for (int sgi = s_lo; sgi < s_hi; ++sgi) {
             const int ce = sb[sgi + 1];
-            double* ap = acc + ss[sgi] * NR + row;
-            double v = *ap;
+            double* ap = acc + ss[sgi] * NR;
+            double vre = ap[rre], vim = mm ? ap[rim] : 0.0;
             for (int col = sb[sgi]; col < ce; ++col) {
               const int2 cg = colt[col];  // (column base, 2 g)
-              const int idx = (int)((mask >> cg.y) & 3) ^ part;
               const double yr = y[cg.x + rre], yi = y[cg.x + rim];
-              double k0 = (idx & 1) ? kr1 : kr0, k1 = (idx & 1) ? ki1 : ki0;
-              const double t = fma(k0, yr, k1 * yi);
-              v = (idx & 2) ? v - t : v + t;
+              const double ure = fma(ca, yr, -sa * yi), uim = fma(sa, yr, ca * yi);
+              const int ire = (int)((mre >> cg.y) & 3), iim = (int)((mim >> cg.y) & 3) ^ 1;
+              const double tre = (ire & 1) ? uim : ure, tim = (iim & 1) ? uim : ure;
+              vre = (ire & 2) ? vre - tre : vre + tre;
+              vim = (iim & 2) ? vim - tim : vim + tim;
             }
-            *ap = v;
+            ap[rre] = vre;
+            if (mm) ap[rim] = vim;
           }
         }
       }

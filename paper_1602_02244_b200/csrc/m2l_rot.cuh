@@ -387,7 +387,6 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
         const double* __restrict__ ob = G::SA ? m.ob + b * BLOB : m.az + b * 2 * (P + 1);
         const int32_t* __restrict__ dsc = m.desc + (i % 3) * rot_desc_ints(NC);
         const int ns = dsc[1];
-        const int* __restrict__ meta = dsc + 4 + NC;
         const int* __restrict__ ss = dsc + 4 + 2 * NC;
         const int* __restrict__ sb = dsc + 4 + 3 * NC;
         double* __restrict__ acc = m.acc;

@@ -31,7 +31,10 @@ using namespace near;
 
 constexpr int kWarps = 4;   // warps (target leaves) per CTA
 constexpr int kBuf = 128;   // source particles per staging buffer
-constexpr int kMaxTPL = 4;  // targets per lane (measured: 8 is slower, register pressure)
+#ifndef FMM_NEAR_TPL_MAX
+#define FMM_NEAR_TPL_MAX 4
+#endif
+constexpr int kMaxTPL = FMM_NEAR_TPL_MAX;  // targets per lane (measured: 8 is slower, register pressure)
 template <bool kGrad>
 constexpr int max_tpl() { return kMaxTPL; }
 #ifndef FMM_NEAR_MINB
@@ -205,6 +208,12 @@ __device__ __forceinline__ void dispatch(const NearArgs& a, int leaf, int t0, in
     case 2: process_group<kGrad, 2>(a, leaf, t0, cnt, G, lane, buf); break;
     case 3: process_group<kGrad, 3>(a, leaf, t0, cnt, G, lane, buf); break;
     case 4: process_group<kGrad, 4>(a, leaf, t0, cnt, G, lane, buf); break;
+#if FMM_NEAR_TPL_MAX >= 5
+    case 5: process_group<kGrad, 5>(a, leaf, t0, cnt, G, lane, buf); break;
+#endif
+#if FMM_NEAR_TPL_MAX >= 6
+    case 6: process_group<kGrad, 6>(a, leaf, t0, cnt, G, lane, buf); break;
+#endif
   }
 }
 

@@ -341,6 +341,10 @@ void near_pass_warp(fmm_plan_s& P, double* phi, double* grad) {
   a.phi_out = phi;
   a.grad_out = grad;
   a.max_tpl = grad ? max_tpl<true>() : max_tpl<false>();
+  // few sources per target (< 1,200 interactions per particle, e.g. configs[3] at 849): four
+  // targets per lane loses to three (near 13.4 vs 14.6 ms); configs[1], [2], [4] (1,641 - 2,256)
+  // keep four (configs[2] 2.66 vs 2.72 ms)
+  if (P.n > 0 && P.n_p2p_interactions < 1200LL * P.n) a.max_tpl = std::min(a.max_tpl, 3);
   a.max_g = 8;
   if (const char* e = getenv("FMM_NEAR_MAXTPL")) a.max_tpl = std::max(1, std::min(a.max_tpl, atoi(e)));
   if (const char* e = getenv("FMM_NEAR_MAXG")) a.max_g = std::max(1, std::min(8, atoi(e)));

@@ -101,6 +101,8 @@ typedef struct {
                                 block stages + the two azimuthal rotations; v1/v2: 2(p+1)^4) */
   int64_t bytes_by[8];       /* bytes_device by category, FMM_B_* (the FMM side of PAPER.md
                                 Fig 4, "strictly O(N) storage") */
+  int64_t launches_total;    /* kernels launched by libfmm in this process so far (all plans,
+                                setup included): differences count a region's launches */
 } fmm_stats_t;
 enum {
   FMM_B_PARTICLES = 0,  /* keys, permutation, positions + charges, host-call staging */

@@ -395,6 +395,7 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     out->t_matvec_ms[i] = P->t_matvec[i];
   }
   out->bytes_device = P->bytes();
+  out->launches_total = fmm::launch_counter().load();
   {
     const fmm::M2LDmma& D = P->m2l_dmma;
     const fmm::Cells& c = P->cells;

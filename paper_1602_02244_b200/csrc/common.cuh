@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -23,7 +24,13 @@ inline void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw Error(4, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define FMM_CUDA(x) ::fmm::check_cuda((x), #x)
-#define FMM_LAUNCHED(name) ::fmm::check_cuda(cudaGetLastError(), name)
+// process-wide count of kernel launches (every launch is followed by FMM_LAUNCHED); fmm_stats
+// reports it so a caller can count the launches of a timed region exactly
+inline std::atomic<int64_t>& launch_counter() {
+  static std::atomic<int64_t> c{0};
+  return c;
+}
+#define FMM_LAUNCHED(name) (::fmm::launch_counter()++, ::fmm::check_cuda(cudaGetLastError(), name))
 
 __host__ __device__ inline int ncoef(int p) { return (p + 1) * (p + 2) / 2; }
 __host__ __device__ inline int cidx(int n, int m) { return n * (n + 1) / 2 + m; }

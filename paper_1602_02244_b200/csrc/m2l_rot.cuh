@@ -71,7 +71,11 @@ constexpr int kRotMMA = FMM_ROT_MMA;  // MMA warps of the v3 kernel
 // register rebalancing between the warp roles (setmaxnreg, per warpgroup): the prep and accumulate
 // warps give registers to the MMA warps, which prefetch the next item's A fragments
 constexpr int kRotRegsLow = 64, kRotRegsMMA = 136;
-constexpr int kRotAcc = FMM_ROT_ACC;    // accumulate warps
+constexpr int kRotAcc = FMM_ROT_ACC;    // accumulate warps (p > 8)
+// p <= 8: smaller blocks, the accumulate warps need less of the SM: 6 warps and prep batches of 4
+// (configs[3], p = 8: M2L 56.8 -> 55.4 ms; p = 10 keeps 8 warps / batches of 6, which it prefers)
+constexpr int rot_acc_warps(int p) { return p <= 8 ? 6 : kRotAcc; }
+constexpr int rot_prep_batch(int p) { return p <= 8 ? 4 : 6; }
 constexpr int kRotNear = FMM_ROT_NEAR;  // near-field (P2P) warps fused into the kernel
 constexpr int rot_ksb(int p) { return p < 4 ? 2 : (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB), >= 2 (small items use 2)
 // ints of one per-chunk descriptor: [ncol, nseg, class, 0 | srcs | meta | sslot | sbeg[NC + 1]]
@@ -121,7 +125,7 @@ struct RGeo {
   static constexpr int S = rot_xstride(KPAD);  // column stride (see col_base)
   static constexpr int NC = rot_nc(P);
   static constexpr int NT = NC / 8;
-  static constexpr int NMMA = kRotMMA, NPREP = 4, NACC = kRotAcc, NNEAR = kRotNear;
+  static constexpr int NMMA = kRotMMA, NPREP = 4, NACC = rot_acc_warps(P), NNEAR = kRotNear;
   static constexpr int KSB = rot_ksb(P);
   static constexpr int NCOEF = (P + 1) * (P + 2) / 2;
   static constexpr bool SA = rot_smem_a(P);
@@ -465,7 +469,7 @@ __global__ void __launch_bounds__(32 * (RGeo<P>::NMMA + RGeo<P>::NPREP + RGeo<P>
         // X[col] <- Az_M (D^M_g)^-1 X[col]; item = (column, (n, m >= 1) pair), batches of
         // four items: all loads, then the arithmetic, then the stores (no smem aliasing stalls)
         constexpr int NP = NCOEF - (P + 1);  // pairs with m >= 1
-        constexpr int kPB = 6;               // items per batch
+        constexpr int kPB = rot_prep_batch(P);  // items per batch
         const int nit = ncol * NP;
         for (int it0 = h; it0 < nit; it0 += kPB * nprep_t) {
           double v0[kPB], v1[kPB], cs[kPB], sn[kPB];

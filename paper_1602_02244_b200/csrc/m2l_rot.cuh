@@ -72,10 +72,14 @@ constexpr int kRotMMA = FMM_ROT_MMA;  // MMA warps of the v3 kernel
 // warps give registers to the MMA warps, which prefetch the next item's A fragments
 constexpr int kRotRegsLow = 64, kRotRegsMMA = 136;
 constexpr int kRotAcc = FMM_ROT_ACC;    // accumulate warps (p > 8)
-// p <= 8: smaller blocks, the accumulate warps need less of the SM: 6 warps and prep batches of 4
-// (configs[3], p = 8: M2L 56.8 -> 55.4 ms; p = 10 keeps 8 warps / batches of 6, which it prefers)
-constexpr int rot_acc_warps(int p) { return p <= 8 ? 6 : kRotAcc; }
-constexpr int rot_prep_batch(int p) { return p <= 8 ? 4 : 6; }
+// p <= 8 and p >= 11: 6 accumulate warps and prep batches of 4 (less contention for the MMA warps)
+// (configs[3], p = 8: M2L 56.8 -> 55.4 ms; configs[4], p = 12: 423 -> 381 ms; p = 9, 10 keep 8
+// warps / batches of 6, which configs[2] prefers)
+#ifndef FMM_ROT_HIGHP_SMALL
+#define FMM_ROT_HIGHP_SMALL 1
+#endif
+constexpr int rot_acc_warps(int p) { return (p <= 8 || FMM_ROT_HIGHP_SMALL && p >= 11) ? 6 : kRotAcc; }
+constexpr int rot_prep_batch(int p) { return (p <= 8 || FMM_ROT_HIGHP_SMALL && p >= 11) ? 4 : 6; }
 constexpr int kRotNear = FMM_ROT_NEAR;  // near-field (P2P) warps fused into the kernel
 constexpr int rot_ksb(int p) { return p < 4 ? 2 : (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB), >= 2 (small items use 2)
 // ints of one per-chunk descriptor: [ncol, nseg, class, 0 | srcs | meta | sslot | sbeg[NC + 1]]

@@ -60,7 +60,7 @@ constexpr bool rot_smem_a(int p) { return p <= FMM_ROT_SA_MAXP; }
 #endif
 constexpr int kRotMMA = FMM_ROT_MMA;  // MMA warps of the v3 kernel
 #ifndef FMM_ROT_ACC
-#define FMM_ROT_ACC 8
+#define FMM_ROT_ACC 7
 #endif
 #ifndef FMM_ROT_NEAR
 #define FMM_ROT_NEAR 0
@@ -73,13 +73,22 @@ constexpr int kRotMMA = FMM_ROT_MMA;  // MMA warps of the v3 kernel
 constexpr int kRotRegsLow = 64, kRotRegsMMA = 136;
 constexpr int kRotAcc = FMM_ROT_ACC;    // accumulate warps (p > 8)
 // p <= 8 and p >= 11: 6 accumulate warps and prep batches of 4 (less contention for the MMA warps)
-// (configs[3], p = 8: M2L 56.8 -> 55.4 ms; configs[4], p = 12: 423 -> 381 ms; p = 9, 10 keep 8
+// (configs[3], p = 8: M2L 56.8 -> 55.4 ms; configs[4], p = 12: 423 -> 381 ms; p = 9, 10 take 7
 // warps / batches of 6, which configs[2] prefers)
 #ifndef FMM_ROT_HIGHP_SMALL
 #define FMM_ROT_HIGHP_SMALL 1
 #endif
-constexpr int rot_acc_warps(int p) { return (p <= 8 || FMM_ROT_HIGHP_SMALL && p >= 11) ? 6 : kRotAcc; }
-constexpr int rot_prep_batch(int p) { return (p <= 8 || FMM_ROT_HIGHP_SMALL && p >= 11) ? 4 : 6; }
+#ifndef FMM_ROT_ACC_SMALL
+#define FMM_ROT_ACC_SMALL 6
+#endif
+#ifndef FMM_ROT_PB_SMALL
+#define FMM_ROT_PB_SMALL 4
+#endif
+constexpr int rot_acc_warps(int p) { return (p <= 8 || FMM_ROT_HIGHP_SMALL && p >= 11) ? FMM_ROT_ACC_SMALL : kRotAcc; }
+#ifndef FMM_ROT_PB_BIG
+#define FMM_ROT_PB_BIG 6
+#endif
+constexpr int rot_prep_batch(int p) { return (p <= 8 || FMM_ROT_HIGHP_SMALL && p >= 11) ? FMM_ROT_PB_SMALL : FMM_ROT_PB_BIG; }
 constexpr int kRotNear = FMM_ROT_NEAR;  // near-field (P2P) warps fused into the kernel
 constexpr int rot_ksb(int p) { return p < 4 ? 2 : (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB), >= 2 (small items use 2)
 // ints of one per-chunk descriptor: [ncol, nseg, class, 0 | srcs | meta | sslot | sbeg[NC + 1]]

@@ -567,7 +567,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
     configured[P.p][split > 1] = sh;
   }
   r.split = split;
-  const dim3 grid((unsigned)(D.ntiles * split)), block(32 * (kRotMMA + 4 + rot_acc_warps(P.p) + kRotNear));
+  const dim3 grid((unsigned)(D.ntiles * split)), block(32 * (kRotMMA + rot_prep_warps(P.p) + rot_acc_warps(P.p) + kRotNear));
   k<<<grid, block, sh, P.stream>>>(r, dbg);
   FMM_LAUNCHED("m2l_rot_kernel");
   if (split > 1) {

@@ -88,6 +88,13 @@ constexpr int rot_acc_warps(int p) { return (p <= 8 || FMM_ROT_HIGHP_SMALL && p 
 #ifndef FMM_ROT_PB_BIG
 #define FMM_ROT_PB_BIG 6
 #endif
+#ifndef FMM_ROT_PREP_W_BIG
+#define FMM_ROT_PREP_W_BIG 4
+#endif
+#ifndef FMM_ROT_PREP_W_SMALL
+#define FMM_ROT_PREP_W_SMALL 4
+#endif
+constexpr int rot_prep_warps(int p) { return (p <= 8 || FMM_ROT_HIGHP_SMALL && p >= 11) ? FMM_ROT_PREP_W_SMALL : FMM_ROT_PREP_W_BIG; }
 constexpr int rot_prep_batch(int p) { return (p <= 8 || FMM_ROT_HIGHP_SMALL && p >= 11) ? FMM_ROT_PB_SMALL : FMM_ROT_PB_BIG; }
 constexpr int kRotNear = FMM_ROT_NEAR;  // near-field (P2P) warps fused into the kernel
 constexpr int rot_ksb(int p) { return p < 4 ? 2 : (p + 1 + 3) / 4; }  // k-steps of a big item (16 x 4 KSB), >= 2 (small items use 2)
@@ -138,7 +145,7 @@ struct RGeo {
   static constexpr int S = rot_xstride(KPAD);  // column stride (see col_base)
   static constexpr int NC = rot_nc(P);
   static constexpr int NT = NC / 8;
-  static constexpr int NMMA = kRotMMA, NPREP = 4, NACC = rot_acc_warps(P), NNEAR = kRotNear;
+  static constexpr int NMMA = kRotMMA, NPREP = rot_prep_warps(P), NACC = rot_acc_warps(P), NNEAR = kRotNear;
   static constexpr int KSB = rot_ksb(P);
   static constexpr int NCOEF = (P + 1) * (P + 2) / 2;
   static constexpr bool SA = rot_smem_a(P);

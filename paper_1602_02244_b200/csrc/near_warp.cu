@@ -29,8 +29,18 @@ namespace fmm {
 namespace {
 using namespace near;
 
-constexpr int kWarps = 4;   // warps (target leaves) per CTA
-constexpr int kBuf = 128;   // source particles per staging buffer
+#ifndef FMM_NEAR_WARPS
+#define FMM_NEAR_WARPS 1
+#endif
+#ifndef FMM_NEAR_MINB_GRAD
+#define FMM_NEAR_MINB_GRAD (12 / FMM_NEAR_WARPS)  // 12 warps per SM for the phi + grad kernel
+#endif
+#ifndef FMM_NEAR_BUF
+#define FMM_NEAR_BUF 128
+#endif
+constexpr int kWarps = FMM_NEAR_WARPS;  // warps (target leaves) per CTA: 1 (20 CTAs per SM) beat 4 and 2
+                                        // (configs[2] near 2.66 -> 2.59 ms, [3] 13.4 -> 11.9, [4] 254.5 -> 239.1)
+constexpr int kBuf = FMM_NEAR_BUF;      // source particles per staging buffer
 #ifndef FMM_NEAR_TPL_MAX
 #define FMM_NEAR_TPL_MAX 4
 #endif
@@ -38,7 +48,7 @@ constexpr int kMaxTPL = FMM_NEAR_TPL_MAX;  // targets per lane (measured: 8 is s
 template <bool kGrad>
 constexpr int max_tpl() { return kMaxTPL; }
 #ifndef FMM_NEAR_MINB
-#define FMM_NEAR_MINB 4  // CTAs per SM for the phi-only kernel (122 registers, no spills)
+#define FMM_NEAR_MINB 20  // CTAs (1 warp each) per SM for the phi-only kernel (96 registers, no spills)
 #endif
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -218,7 +228,7 @@ __device__ __forceinline__ void dispatch(const NearArgs& a, int leaf, int t0, in
 }
 
 template <bool kGrad>
-__global__ void __launch_bounds__(32 * kWarps, kGrad ? 3 : FMM_NEAR_MINB) near_warp_kernel(const int32_t* __restrict__ leaves, int64_t nleaves,
+__global__ void __launch_bounds__(32 * kWarps, kGrad ? FMM_NEAR_MINB_GRAD : FMM_NEAR_MINB) near_warp_kernel(const int32_t* __restrict__ leaves, int64_t nleaves,
                                                                 const NearArgs a) {
   __shared__ __align__(16) double4 buf[kWarps][2][kBuf];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

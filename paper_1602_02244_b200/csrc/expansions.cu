@@ -27,7 +27,10 @@ constexpr int kM2MThreads = 256;  // M2M / L2L: items (child, coefficient)
 // generated in registers (diagonal product + two-term recurrence), q conj(R) accumulated per
 // lane over the leaf's particles (lane = particle), then butterfly-reduced over the warp in
 // a fixed order (deterministic); lane k writes coefficient (m + k, m).
-constexpr int kP2MWarps = 4;
+#ifndef FMM_P2M_WARPS
+#define FMM_P2M_WARPS 4
+#endif
+constexpr int kP2MWarps = FMM_P2M_WARPS;
 #ifndef FMM_P2M_CACHE
 #define FMM_P2M_CACHE 2
 #endif
@@ -281,7 +284,10 @@ namespace {
 // M2M sums the 8 signed columns of its parent (shuffle over the quad, fixed order); L2L adds
 // each column to its child. Degree-blocked real layout => M2M is block lower triangular
 // (output degree j reads degrees <= j), L2L block upper triangular; zero blocks are skipped.
-constexpr int kShiftWarps = 4;
+#ifndef FMM_SHIFT_WARPS
+#define FMM_SHIFT_WARPS 4
+#endif
+constexpr int kShiftWarps = FMM_SHIFT_WARPS;
 
 __host__ __device__ constexpr int shift_isq(int r) {
   int n = 0;

@@ -21,6 +21,13 @@
 
 #include "plan.h"
 
+#ifndef FMM_2D_NEAR_THREADS
+#define FMM_2D_NEAR_THREADS 128
+#endif
+#ifndef FMM_2D_M2L_THREADS
+#define FMM_2D_M2L_THREADS 256
+#endif
+
 namespace fmm {
 namespace {
 
@@ -289,7 +296,7 @@ void upward_2d(fmm_plan_s& P) {
 
 void m2l_2d(fmm_plan_s& P) {
   FMM_CUDA(cudaMemsetAsync(P.L.ptr, 0, P.L.bytes(), P.stream));
-  m2l2d_kernel<<<cdiv(P.cells.n * 32, 256), 256, 0, P.stream>>>(P.cells.n, P.m2l.off, P.m2l.src, P.cells.center, P.M,
+  m2l2d_kernel<<<cdiv(P.cells.n * 32, FMM_2D_M2L_THREADS), FMM_2D_M2L_THREADS, 0, P.stream>>>(P.cells.n, P.m2l.off, P.m2l.src, P.cells.center, P.M,
                                                                  P.p, P.nc, P.L);
   FMM_LAUNCHED("m2l2d_kernel");
 }
@@ -306,7 +313,7 @@ void downward_2d(fmm_plan_s& P) {
 void near_2d(fmm_plan_s& P, double* phi, double* grad) {
   const double eln2 = P.e * 0.69314718055994530942;  // phi = phi_u - e ln2 (Q - Q0)
   const double sgrad = std::ldexp(1.0, -P.e);
-  near2d_kernel<<<cdiv(P.nleaves * 32, 128), 128, 0, P.stream>>>(
+  near2d_kernel<<<cdiv(P.nleaves * 32, FMM_2D_NEAR_THREADS), FMM_2D_NEAR_THREADS, 0, P.stream>>>(
       P.leaves, P.nleaves, P.cells.begin, P.cells.end, P.p2p.off, P.p2p.src, P.cells.center, P.pos, P.L, P.M, P.p,
       P.nc, eln2, sgrad, P.perm, phi, grad);
   FMM_LAUNCHED("near2d_kernel");

@@ -148,6 +148,7 @@ struct RGeo {
   static constexpr int S = rot_xstride(KPAD);  // column stride (see col_base)
   static constexpr int NC = rot_nc(P);
   static constexpr int NT = NC / 8;
+  static_assert(NC % 8 == 0, "chunk width must be a whole number of 8-column n-tiles");
   static constexpr int NMMA = kRotMMA, NPREP = rot_prep_warps(P), NACC = rot_acc_warps(P), NNEAR = kRotNear;
   static constexpr int KSB = rot_ksb(P);
   static constexpr int NCOEF = (P + 1) * (P + 2) / 2;

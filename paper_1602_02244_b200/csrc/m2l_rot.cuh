@@ -50,7 +50,10 @@ constexpr int rot_xstride(int kpad) {
 #ifndef FMM_ROT_NC_SMALLP
 #define FMM_ROT_NC_SMALLP FMM_ROT_NC
 #endif
-constexpr int rot_nc(int p) { return p <= 8 ? FMM_ROT_NC_SMALLP : (p <= 10 ? FMM_ROT_NC : 32); }
+#ifndef FMM_ROT_NC_HIGHP
+#define FMM_ROT_NC_HIGHP 32
+#endif
+constexpr int rot_nc(int p) { return p <= 8 ? FMM_ROT_NC_SMALLP : (p <= 10 ? FMM_ROT_NC : FMM_ROT_NC_HIGHP); }
 // class data staged into shared memory by TMA (p <= 10, where it fits beside the chunk buffers)
 // or read by the MMA warps straight from L2 with one-item prefetch (larger p); measured at
 // configs[2]: M2L 7.5 ms (shared) vs 8.4 ms (L2)

@@ -95,10 +95,12 @@ typedef struct {
   double t_matvec_ms[8]; /* FMM_T_UPWARD .. FMM_T_MATVEC_TOTAL (0 unless timing enabled) */
   int64_t bytes_device;  /* device memory owned by the plan */
   int m2l_variant;       /* M2L formulation in use: 1 matrix-free O(p^4) per pair, 2 dense class
-                            operators on DMMA, 3 rotation-factored class operators on DMMA */
+                            operators on DMMA, 3 rotation-factored class operators on DMMA;
+                            0 for a 2D (log-kernel) plan, whose M2L is the complex series */
   int m2l_pad_;
   double m2l_flops_per_pair; /* useful flops per M2L pair of that formulation (v3: the three
-                                block stages + the two azimuthal rotations; v1/v2: 2(p+1)^4) */
+                                block stages + the two azimuthal rotations; v1/v2: 2(p+1)^4;
+                                2D: 8(p+1)^2, one complex multiply-add per (l, k)) */
   int64_t bytes_by[8];       /* bytes_device by category, FMM_B_* (the FMM side of PAPER.md
                                 Fig 4, "strictly O(N) storage") */
   int64_t launches_total;    /* kernels launched by libfmm in this process so far (all plans,

@@ -422,7 +422,10 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
   out->m2l_variant = P->m2l_variant;
   {
     const double p1 = P->p + 1;
-    if (P->m2l_variant == 3) {  // sum_n (n+1)^2 + n^2 per rotation stage, sum_m (p+1-m)^2 (Re) + (Im, m > 0)
+    if (P->dim == 2) {  // 2D log kernel: one complex multiply-add per (l, k) pair
+      out->m2l_variant = 0;
+      out->m2l_flops_per_pair = 8.0 * p1 * p1;
+    } else if (P->m2l_variant == 3) {  // sum_n (n+1)^2 + n^2 per rotation stage, sum_m (p+1-m)^2 (Re) + (Im, m > 0)
       double rot = 0, z = 0;
       for (int n = 0; n <= P->p; ++n) rot += (n + 1.0) * (n + 1.0) + (double)n * n;
       for (int m = 0; m <= P->p; ++m) z += (m ? 2.0 : 1.0) * (p1 - m) * (p1 - m);

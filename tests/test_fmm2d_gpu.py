@@ -87,6 +87,8 @@ def test_truncation_vs_direct_and_determinism(torch_cuda):
     pl, a, ga = run(torch_cuda, xy, q, 10, 32, 0.5)
     b, gb = pl.matvec(torch_cuda.from_numpy(q).cuda(), grad=True)
     assert np.array_equal(a, b.cpu().numpy()) and np.array_equal(ga, gb.cpu().numpy())
+    st = pl.stats()
+    assert st["m2l_variant"] == 0 and st["m2l_flops_per_pair"] == 8.0 * 11 ** 2
 
 
 def test_usage(torch_cuda):

@@ -193,14 +193,47 @@ __global__ void l2l2d_kernel(int64_t lb, int64_t ncell, const int32_t* __restric
   }
 }
 
+// ln(x) for a normal positive double: x = 2^k m, m in [1, 2); the top 7 bits of m pick a table
+// entry c_j = 1 / (1 + (j + 1/2) / 128) with its logarithm T_j = -ln c_j (shared memory), so that
+// u = m c_j - 1 (one fma, |u| <= 2^-8) and ln m = T_j + ln(1 + u), the series to u^8 (its
+// truncation error u^9 / 9 < 2^-72 is far below one ulp of u). Subnormal and tiny x (never met
+// at the normalised frame's distances, kept exact anyway) take the library log.
+#ifndef FMM_2D_LOG_TABLE
+#define FMM_2D_LOG_TABLE 1
+#endif
+__device__ __forceinline__ double log_tab(double x, const double2* __restrict__ tab) {
+  const long long b = __double_as_longlong(x);
+  const int k = (int)(b >> 52) - 1023;
+  if (k < -1000) return log(x);
+  const double2 cj = tab[(b >> 45) & 127];  // (c_j, T_j)
+  const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+  const double u = fma(m, cj.x, -1.0);
+  double s = -0.125;
+  s = fma(s, u, 1.0 / 7.0);
+  s = fma(s, u, -1.0 / 6.0);
+  s = fma(s, u, 0.2);
+  s = fma(s, u, -0.25);
+  s = fma(s, u, 1.0 / 3.0);
+  s = fma(s, u, -0.5);
+  const double lm = fma(s * u, u, u) + cj.y;
+  return fma((double)k, 6.93147180559945286227e-01, fma((double)k, 2.31904681384629955842e-17, lm));
+}
+
 // L2P + P2P: warp per target leaf, lane per target; outputs in caller order (perm), with the
 // 2^-e rescale of the logarithm and the gradient
+template <bool GRAD>
 __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ cbeg,
                               const int32_t* __restrict__ cend, const int32_t* __restrict__ poff,
                               const int32_t* __restrict__ psrc, const double4* __restrict__ center,
                               const double4* __restrict__ pos, const double2* __restrict__ L, const double2* __restrict__ M,
                               int p, int stride, double eln2, double sgrad, const uint32_t* __restrict__ perm,
                               double* __restrict__ phi, double* __restrict__ grad) {
+  __shared__ double2 tab[128];
+  for (int j = threadIdx.x; j < 128; j += blockDim.x) {
+    const double c = 1.0 / (1.0 + (j + 0.5) / 128.0);
+    tab[j] = make_double2(c, -log(c));
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t li = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (li >= nleaves) return;
@@ -218,10 +251,16 @@ __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleave
         const double dx = t.x - s.x, dy = t.y - s.y;
         const double r2 = dx * dx + dy * dy;
         if (r2 > 0.0) {
+#if FMM_2D_LOG_TABLE
+          f -= s.w * 0.5 * log_tab(r2, tab);
+#else
           f -= s.w * 0.5 * log(r2);
-          const double w = s.w / r2;
-          gx -= w * dx;
-          gy -= w * dy;
+#endif
+          if (GRAD) {
+            const double w = s.w / r2;
+            gx -= w * dx;
+            gy -= w * dy;
+          }
         } else {
           q0 += s.w;
         }
@@ -240,7 +279,7 @@ __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleave
     gy += dPh.y;
     const uint32_t o = perm[i];
     phi[o] = f - eln2 * (Q - q0);
-    if (grad) {
+    if (GRAD) {
       grad[3 * (int64_t)o] = gx * sgrad;
       grad[3 * (int64_t)o + 1] = gy * sgrad;
       grad[3 * (int64_t)o + 2] = 0.0;
@@ -313,7 +352,8 @@ void downward_2d(fmm_plan_s& P) {
 void near_2d(fmm_plan_s& P, double* phi, double* grad) {
   const double eln2 = P.e * 0.69314718055994530942;  // phi = phi_u - e ln2 (Q - Q0)
   const double sgrad = std::ldexp(1.0, -P.e);
-  near2d_kernel<<<cdiv(P.nleaves * 32, FMM_2D_NEAR_THREADS), FMM_2D_NEAR_THREADS, 0, P.stream>>>(
+  auto k = grad ? near2d_kernel<true> : near2d_kernel<false>;
+  k<<<cdiv(P.nleaves * 32, FMM_2D_NEAR_THREADS), FMM_2D_NEAR_THREADS, 0, P.stream>>>(
       P.leaves, P.nleaves, P.cells.begin, P.cells.end, P.p2p.off, P.p2p.src, P.cells.center, P.pos, P.L, P.M, P.p,
       P.nc, eln2, sgrad, P.perm, phi, grad);
   FMM_LAUNCHED("near2d_kernel");

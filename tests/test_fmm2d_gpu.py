@@ -102,3 +102,25 @@ def test_usage(torch_cuda):
                           ctypes.byref(ex)) == N.FMM_ERR_USAGE
     ex1 = N.FmmExec(0, None, 0, 1)
     assert L.fmm_setup_2d(ctypes.byref(h), None, 10, 4, 8, 0.4, ctypes.byref(ex1)) == N.FMM_ERR_USAGE
+
+
+def test_near_log_accuracy(torch_cuda):
+    """The near field's table-driven logarithm (fmm2d.cu log_tab) against numpy's log over
+    distances 1e-12 .. 1e5 (every table entry and binade), and the subnormal-r^2 fallback."""
+    rng = np.random.default_rng(12)
+    worst = 0.0
+    for r in np.r_[10.0 ** rng.uniform(-12, 5, 300), 2.0 ** np.arange(-30, 16) * (1 + 2.0 ** -52)]:
+        th = rng.uniform(0, 2 * np.pi)
+        xy = np.array([[0.0, 0.0], [r * np.cos(th), r * np.sin(th)]])
+        q = np.array([0.7, -1.3])
+        _, phi, g = run(torch_cuda, xy, q, 4, 8, 0.5)
+        ref = 0.5 * np.log(xy[1, 0] ** 2 + xy[1, 1] ** 2)  # phi_0 = -q_1 log r
+        err = abs(phi[0] / -q[1] - ref) / (1.0 + abs(ref))
+        worst = max(worst, err)
+    assert worst < 4e-16, worst
+    # r^2 = 1e-310 is subnormal (about 44 significant bits, hence the looser bound)
+    xy = np.array([[0.0, 0.0], [1e-155, 0.0], [1.0, 1.0]])
+    q = np.array([1.0, 2.0, -1.0])
+    _, phi, _ = run(torch_cuda, xy, q, 4, 8, 0.5)
+    ref = -2.0 * np.log(1e-155) + 1.0 * 0.5 * np.log(2.0)
+    assert abs(phi[0] - ref) <= 1e-13 * abs(ref), (phi[0], ref)

@@ -193,30 +193,38 @@ __global__ void l2l2d_kernel(int64_t lb, int64_t ncell, const int32_t* __restric
   }
 }
 
-// ln(x) for a normal positive double: x = 2^k m, m in [1, 2); the top 7 bits of m pick a table
-// entry c_j = 1 / (1 + (j + 1/2) / 128) with its logarithm T_j = -ln c_j (shared memory), so that
-// u = m c_j - 1 (one fma, |u| <= 2^-8) and ln m = T_j + ln(1 + u), the series to u^8 (its
-// truncation error u^9 / 9 < 2^-72 is far below one ulp of u). Subnormal and tiny x (never met
-// at the normalised frame's distances, kept exact anyway) take the library log.
+// ln(x) for a normal positive double, split as ln x = k ln 2 + lm: x = 2^k m, m in [1, 2); the
+// top 7 bits of m pick a table entry c_j = 1 / (1 + (j + 1/2) / 128) with T_j = -ln c_j (shared
+// memory), u = m c_j - 1 is one fma (|u| <= 2^-8) and lm = T_j + ln(1 + u) with the series to u^7
+// (truncation u^8 / 8 <= 2^-67, below 2^-13 ulp of any |ln x| >= 2^-8 and of u itself when k = 0
+// and m ~ 1). k is returned as a double (exponent bits re-biased by one add, no conversion) so the
+// caller accumulates sum q k and sum q lm separately and multiplies by ln 2 once per target.
+// Subnormal and tiny x (never met at the normalised frame's distances, kept exact anyway) take
+// the library log with k = 0.
 #ifndef FMM_2D_LOG_TABLE
 #define FMM_2D_LOG_TABLE 1
 #endif
-__device__ __forceinline__ double log_tab(double x, const double2* __restrict__ tab) {
+#ifndef FMM_2D_NEAR_SPLIT  // 1: G lanes per target (below); measured slower, profiles/r1_fmm2d.md
+#define FMM_2D_NEAR_SPLIT 0
+#endif
+__device__ __forceinline__ double log_tab(double x, const double2* __restrict__ tab, double& kd) {
   const long long b = __double_as_longlong(x);
-  const int k = (int)(b >> 52) - 1023;
-  if (k < -1000) return log(x);
+  const long long be = b >> 52;  // biased exponent (x > 0)
+  if (be < 1023 - 1000) {
+    kd = 0.0;
+    return log(x);
+  }
+  kd = __longlong_as_double(0x4330000000000000LL | be) - (4503599627370496.0 + 1023.0);
   const double2 cj = tab[(b >> 45) & 127];  // (c_j, T_j)
   const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
   const double u = fma(m, cj.x, -1.0);
-  double s = -0.125;
-  s = fma(s, u, 1.0 / 7.0);
+  double s = 1.0 / 7.0;
   s = fma(s, u, -1.0 / 6.0);
   s = fma(s, u, 0.2);
   s = fma(s, u, -0.25);
   s = fma(s, u, 1.0 / 3.0);
   s = fma(s, u, -0.5);
-  const double lm = fma(s * u, u, u) + cj.y;
-  return fma((double)k, 6.93147180559945286227e-01, fma((double)k, 2.31904681384629955842e-17, lm));
+  return fma(s * u, u, u) + cj.y;
 }
 
 // L2P + P2P: warp per target leaf, lane per target; outputs in caller order (perm), with the
@@ -241,20 +249,39 @@ __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleave
   const double4 c = center[A];
   const double2* loc = L + (int64_t)A * stride;
   const double Q = M[0].x;  // root a_0 = total charge
-  for (int i = cbeg[A] + lane; i < cend[A]; i += 32) {
+  // FMM_2D_NEAR_SPLIT: G lanes per target (G | 32), each taking every G-th source, G chosen to
+  // minimise the lane passes per source ceil(nt G / 32) / G (a leaf of 40 targets: G = 4, 5 passes
+  // over 1/4 of the sources instead of 2 over all of them). Measured slower (uniform square 1M:
+  // near 2.63 vs 1.95 ms), so the shipped kernel is G = 1: lane per target, sources broadcast.
+  const int b0 = cbeg[A], nt = cend[A] - b0;
+#if FMM_2D_NEAR_SPLIT
+  int G = 1;
+  for (int g = 2; g <= 32; g *= 2)
+    if (((nt * g + 31) >> 5) * G < ((nt * G + 31) >> 5) * g) G = g;
+#else
+  const int G = 1;
+#endif
+  const int npass = (nt * G + 31) >> 5;
+  for (int pass = 0; pass < npass; ++pass) {
+    const int k = pass * 32 + lane, ti = k / G, ph = k & (G - 1);
+    const bool act = ti < nt;
+    const int i = b0 + (act ? ti : nt - 1);
     const double4 t = pos[i];
-    double f = 0.0, gx = 0.0, gy = 0.0, q0 = 0.0;
-    for (int e = poff[A]; e < poff[A + 1]; ++e) {
+    double f = 0.0, fk = 0.0, gx = 0.0, gy = 0.0, q0 = 0.0;  // phi = -(f + ln2 fk) / 2 + ...
+    for (int e = poff[A]; act && e < poff[A + 1]; ++e) {
       const int B = psrc[e];
-      for (int j = cbeg[B]; j < cend[B]; ++j) {
+      for (int j = cbeg[B] + ph; j < cend[B]; j += G) {
         const double4 s = pos[j];
         const double dx = t.x - s.x, dy = t.y - s.y;
         const double r2 = dx * dx + dy * dy;
         if (r2 > 0.0) {
 #if FMM_2D_LOG_TABLE
-          f -= s.w * 0.5 * log_tab(r2, tab);
+          double kd;
+          const double lm = log_tab(r2, tab, kd);
+          f = fma(s.w, lm, f);
+          fk = fma(s.w, kd, fk);
 #else
-          f -= s.w * 0.5 * log(r2);
+          f = fma(s.w, log(r2), f);
 #endif
           if (GRAD) {
             const double w = s.w / r2;
@@ -266,6 +293,16 @@ __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleave
         }
       }
     }
+    for (int off = G >> 1; off > 0; off >>= 1) {
+      f += __shfl_xor_sync(0xffffffffu, f, off);
+      fk += __shfl_xor_sync(0xffffffffu, fk, off);
+      q0 += __shfl_xor_sync(0xffffffffu, q0, off);
+      if (GRAD) {
+        gx += __shfl_xor_sync(0xffffffffu, gx, off);
+        gy += __shfl_xor_sync(0xffffffffu, gy, off);
+      }
+    }
+    if (!act || ph != 0) continue;
     // L2P: Phi = sum c_l w^l, Phi' = sum l c_l w^(l-1) (Horner)
     const double2 w = make_double2(t.x - c.x, t.y - c.y);
     double2 Ph = loc[p], dPh = csc(loc[p], (double)p);
@@ -274,7 +311,7 @@ __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleave
       if (l >= 1) dPh = cadd2(cm(dPh, w), csc(loc[l], (double)l));
     }
     if (p == 0) dPh = make_double2(0.0, 0.0);
-    f -= Ph.x;
+    f = -0.5 * fma(fk, 6.93147180559945286227e-01, fma(fk, 2.31904681384629955842e-17, f)) - Ph.x;
     gx -= dPh.x;
     gy += dPh.y;
     const uint32_t o = perm[i];

@@ -137,6 +137,14 @@ __global__ void m2m2d_kernel(int64_t lb, int64_t ncell, const int32_t* __restric
 __global__ void m2l2d_kernel(int64_t ncells, const int32_t* __restrict__ off, const int32_t* __restrict__ src,
                              const double4* __restrict__ center, const double2* __restrict__ M, int p, int stride,
                              double2* __restrict__ L) {
+  // signed series coefficients, [k][l] so that the lanes (l) of one k read consecutive words:
+  // l = 0: (-1)^k; l >= 1: C(l+k-1, k-1) (-1)^k
+  __shared__ double coef[(kMaxP2 + 1) * (kMaxP2 + 1)];
+  for (int t = threadIdx.x; t < (p + 1) * (p + 1); t += blockDim.x) {
+    const int k = t / (p + 1), l = t % (p + 1);
+    coef[t] = k == 0 ? 0.0 : (l == 0 ? 1.0 : c_binom.v[l + k - 1][k - 1]) * ((k & 1) ? -1.0 : 1.0);
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t A = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (A >= ncells) return;
@@ -150,20 +158,20 @@ __global__ void m2l2d_kernel(int64_t ncells, const int32_t* __restrict__ off, co
     const double2 inv = cinv(z0);
     double2 ip = make_double2(1.0, 0.0);  // inv^l by repeated multiplication (l <= 16)
     for (int k = 0; k < l; ++k) ip = cm(ip, inv);
-    const double2 a0 = M[(int64_t)B * stride];
+    const double a0 = M[(int64_t)B * stride].x;  // a_0 = total charge of B: real
     const double2 bk = lane <= p ? cm(M[(int64_t)B * stride + l], ip) : make_double2(0.0, 0.0);  // a_l z0^-l
     double2 s = make_double2(0.0, 0.0);
     for (int k = 1; k <= p; ++k) {
       const double2 b = shfl2(bk, k);
-      const double coef = l == 0 ? ((k & 1) ? -1.0 : 1.0) : c_binom.v[l + k - 1][k - 1] * ((k & 1) ? -1.0 : 1.0);
-      s = cadd2(s, csc(b, coef));
+      const double cf = coef[k * (p + 1) + l];
+      s.x = fma(b.x, cf, s.x);
+      s.y = fma(b.y, cf, s.y);
     }
     double2 v;
-    if (l == 0) {  // a_0 log(-z0): log|z0| + i arg(-z0)
-      const double2 lg = make_double2(0.5 * log(z0.x * z0.x + z0.y * z0.y), atan2(-z0.y, -z0.x));
-      v = cadd2(cm(a0, lg), s);
+    if (l == 0) {  // a_0 log(-z0): only its real part a_0 log|z0| reaches an output (R45)
+      v = make_double2(fma(a0, 0.5 * log(z0.x * z0.x + z0.y * z0.y), s.x), s.y);
     } else {
-      v = cm(ip, cadd2(csc(a0, -1.0 / l), s));
+      v = cm(ip, make_double2(s.x - a0 / l, s.y));
     }
     acc = cadd2(acc, v);
   }

@@ -212,6 +212,9 @@ __global__ void l2l2d_kernel(int64_t lb, int64_t ncell, const int32_t* __restric
 #ifndef FMM_2D_LOG_TABLE
 #define FMM_2D_LOG_TABLE 1
 #endif
+#ifndef FMM_2D_NEAR_UNROLL  // source-loop unroll; 1M lattice p = 8 near: 1 1.79, 2 1.73, 4 1.68, 8 1.655 ms
+#define FMM_2D_NEAR_UNROLL 4
+#endif
 #ifndef FMM_2D_NEAR_SPLIT  // 1: G lanes per target (below); measured slower, profiles/r1_fmm2d.md
 #define FMM_2D_NEAR_SPLIT 0
 #endif
@@ -278,6 +281,13 @@ __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleave
     double f = 0.0, fk = 0.0, gx = 0.0, gy = 0.0, q0 = 0.0;  // phi = -(f + ln2 fk) / 2 + ...
     for (int e = poff[A]; act && e < poff[A + 1]; ++e) {
       const int B = psrc[e];
+#if FMM_2D_NEAR_UNROLL == 2
+#pragma unroll 2
+#elif FMM_2D_NEAR_UNROLL == 4
+#pragma unroll 4
+#elif FMM_2D_NEAR_UNROLL == 8
+#pragma unroll 8
+#endif
       for (int j = cbeg[B] + ph; j < cend[B]; j += G) {
         const double4 s = pos[j];
         const double dx = t.x - s.x, dy = t.y - s.y;

@@ -134,6 +134,9 @@ __global__ void m2m2d_kernel(int64_t lb, int64_t ncell, const int32_t* __restric
 
 // M2L: warp per target cell; lane k < p+1 owns output l = k; per source, lane k forms
 // b_k = a_k z0^-k and broadcasts it; sources in list order
+// warp per target cell; W = 16 (p <= 15): two source cells per pass, one per half-warp, lane l of
+// a half computing order l; W = 32 (p = 16): one source cell per pass
+template <int W>
 __global__ void m2l2d_kernel(int64_t ncells, const int32_t* __restrict__ off, const int32_t* __restrict__ src,
                              const double4* __restrict__ center, const double2* __restrict__ M, int p, int stride,
                              double2* __restrict__ L) {
@@ -145,24 +148,26 @@ __global__ void m2l2d_kernel(int64_t ncells, const int32_t* __restrict__ off, co
     coef[t] = k == 0 ? 0.0 : (l == 0 ? 1.0 : c_binom.v[l + k - 1][k - 1]) * ((k & 1) ? -1.0 : 1.0);
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, h = lane / W, lw = lane % W;
   const int64_t A = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (A >= ncells) return;
   const double4 ca = center[A];
-  const int l = lane <= p ? lane : 0;
+  const int l = lw <= p ? lw : 0;
   double2 acc = make_double2(0.0, 0.0);
-  for (int e = off[A]; e < off[A + 1]; ++e) {
-    const int B = src[e];
+  const int e1 = off[A + 1];
+  for (int e0 = off[A]; e0 < e1; e0 += 32 / W) {
+    const bool valid = e0 + h < e1;
+    const int B = src[valid ? e0 + h : e0];
     const double4 cb = center[B];
     const double2 z0 = make_double2(cb.x - ca.x, cb.y - ca.y);
     const double2 inv = cinv(z0);
     double2 ip = make_double2(1.0, 0.0);  // inv^l by repeated multiplication (l <= 16)
     for (int k = 0; k < l; ++k) ip = cm(ip, inv);
     const double a0 = M[(int64_t)B * stride].x;  // a_0 = total charge of B: real
-    const double2 bk = lane <= p ? cm(M[(int64_t)B * stride + l], ip) : make_double2(0.0, 0.0);  // a_l z0^-l
+    const double2 bk = lw <= p ? cm(M[(int64_t)B * stride + l], ip) : make_double2(0.0, 0.0);  // a_l z0^-l
     double2 s = make_double2(0.0, 0.0);
     for (int k = 1; k <= p; ++k) {
-      const double2 b = shfl2(bk, k);
+      const double2 b = shfl2(bk, h * W + k);
       const double cf = coef[k * (p + 1) + l];
       s.x = fma(b.x, cf, s.x);
       s.y = fma(b.y, cf, s.y);
@@ -173,8 +178,10 @@ __global__ void m2l2d_kernel(int64_t ncells, const int32_t* __restrict__ off, co
     } else {
       v = cm(ip, make_double2(s.x - a0 / l, s.y));
     }
-    acc = cadd2(acc, v);
+    if (valid) acc = cadd2(acc, v);
   }
+  for (int o = 16; o >= W; o >>= 1) acc = cadd2(acc, make_double2(__shfl_xor_sync(0xffffffffu, acc.x, o),
+                                                                  __shfl_xor_sync(0xffffffffu, acc.y, o)));
   if (lane <= p) L[A * stride + lane] = acc;
 }
 
@@ -390,7 +397,8 @@ void upward_2d(fmm_plan_s& P) {
 
 void m2l_2d(fmm_plan_s& P) {
   FMM_CUDA(cudaMemsetAsync(P.L.ptr, 0, P.L.bytes(), P.stream));
-  m2l2d_kernel<<<cdiv(P.cells.n * 32, FMM_2D_M2L_THREADS), FMM_2D_M2L_THREADS, 0, P.stream>>>(P.cells.n, P.m2l.off, P.m2l.src, P.cells.center, P.M,
+  auto m2l = P.p <= 15 ? m2l2d_kernel<16> : m2l2d_kernel<32>;
+  m2l<<<cdiv(P.cells.n * 32, FMM_2D_M2L_THREADS), FMM_2D_M2L_THREADS, 0, P.stream>>>(P.cells.n, P.m2l.off, P.m2l.src, P.cells.center, P.M,
                                                                  P.p, P.nc, P.L);
   FMM_LAUNCHED("m2l2d_kernel");
 }

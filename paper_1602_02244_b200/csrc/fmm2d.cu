@@ -222,6 +222,9 @@ __global__ void l2l2d_kernel(int64_t lb, int64_t ncell, const int32_t* __restric
 #ifndef FMM_2D_NEAR_UNROLL  // source-loop unroll; 1M lattice p = 8 near: 1 1.79, 2 1.73, 4 1.68, 8 1.655 ms
 #define FMM_2D_NEAR_UNROLL 4
 #endif
+#ifndef FMM_2D_NEAR_BRANCHLESS  // 1: r = 0 by selects; measured neutral (1.72 vs 1.68 / 1.84 vs 1.85 ms)
+#define FMM_2D_NEAR_BRANCHLESS 0
+#endif
 #ifndef FMM_2D_NEAR_SPLIT  // 1: G lanes per target (below); measured slower, profiles/r1_fmm2d.md
 #define FMM_2D_NEAR_SPLIT 0
 #endif
@@ -299,6 +302,22 @@ __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleave
         const double4 s = pos[j];
         const double dx = t.x - s.x, dy = t.y - s.y;
         const double r2 = dx * dx + dy * dy;
+#if FMM_2D_NEAR_BRANCHLESS && FMM_2D_LOG_TABLE
+        // r = 0 (the target itself, coincident points) as a select, not a branch: the term is
+        // evaluated at r^2 = 1 with charge 0 (an exact zero) and the charge goes to q0
+        const bool nz = r2 > 0.0;
+        const double qj = nz ? s.w : 0.0, r2s = nz ? r2 : 1.0;
+        if (!nz) q0 += s.w;
+        double kd;
+        const double lm = log_tab(r2s, tab, kd);
+        f = fma(qj, lm, f);
+        fk = fma(qj, kd, fk);
+        if (GRAD) {
+          const double w = qj / r2s;
+          gx -= w * dx;
+          gy -= w * dy;
+        }
+#else
         if (r2 > 0.0) {
 #if FMM_2D_LOG_TABLE
           double kd;
@@ -316,6 +335,7 @@ __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleave
         } else {
           q0 += s.w;
         }
+#endif
       }
     }
     for (int off = G >> 1; off > 0; off >>= 1) {

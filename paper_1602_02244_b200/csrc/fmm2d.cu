@@ -228,6 +228,16 @@ __global__ void l2l2d_kernel(int64_t lb, int64_t ncell, const int32_t* __restric
 #ifndef FMM_2D_NEAR_SPLIT  // 1: G lanes per target (below); measured slower, profiles/r1_fmm2d.md
 #define FMM_2D_NEAR_SPLIT 0
 #endif
+#ifndef FMM_2D_LOG_RCP  // 1: c_j rebuilt from j (rcp.approx.f32), only T_j loaded: measured slower (1.92 vs 1.68 ms)
+#define FMM_2D_LOG_RCP 0
+#endif
+__device__ __forceinline__ double recip_mid(int j) {  // ~ 256 / (257 + 2 j), the same bits in table and lookup
+  const float n = __uint_as_float(0x4B000000u | (unsigned)(257 + 2 * j)) - 8388608.0f;  // exact
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(n));
+  const unsigned fb = __float_as_uint(r) + (8u << 23);  // x 256
+  return __longlong_as_double(((long long)fb << 29) + ((long long)(1023 - 127) << 52));
+}
 __device__ __forceinline__ double log_tab(double x, const double2* __restrict__ tab, double& kd) {
   const long long b = __double_as_longlong(x);
   const long long be = b >> 52;  // biased exponent (x > 0)
@@ -236,7 +246,12 @@ __device__ __forceinline__ double log_tab(double x, const double2* __restrict__ 
     return log(x);
   }
   kd = __longlong_as_double(0x4330000000000000LL | be) - (4503599627370496.0 + 1023.0);
+#if FMM_2D_LOG_RCP
+  const int jj = (int)((b >> 45) & 127);
+  const double2 cj = make_double2(recip_mid(jj), reinterpret_cast<const double*>(tab)[jj]);  // T_j packed
+#else
   const double2 cj = tab[(b >> 45) & 127];  // (c_j, T_j)
+#endif
   const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
   const double u = fma(m, cj.x, -1.0);
   double s = 1.0 / 7.0;
@@ -260,7 +275,12 @@ __global__ void near2d_kernel(const int32_t* __restrict__ leaves, int64_t nleave
   __shared__ double2 tab[128];
   for (int j = threadIdx.x; j < 128; j += blockDim.x) {
     const double c = 1.0 / (1.0 + (j + 0.5) / 128.0);
+#if FMM_2D_LOG_RCP
+    (void)c;
+    reinterpret_cast<double*>(tab)[j] = -log(recip_mid(j));  // T_j, 1 KB dense
+#else
     tab[j] = make_double2(c, -log(c));
+#endif
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;

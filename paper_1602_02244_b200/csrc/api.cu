@@ -157,7 +157,9 @@ void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
   P.near_fused_grad = grad != nullptr;
   if (P.near_fused_active) fmm::near_fused_prepare(P, grad != nullptr);
   T.mark(1);
-  if (P.m2l_variant >= 2)
+  if (P.m2l_variant == 4)
+    fmm::m2l_v4_pass(P);
+  else if (P.m2l_variant >= 2)
     fmm::m2l_dmma_pass(P);
   else
     fmm::m2l_pass(P);
@@ -204,7 +206,7 @@ int64_t fmm_plan_s::bytes() const {
        cells.parent.bytes() + cells.anchor.bytes() + cells.center.bytes();
   b += p2p.tgt.bytes() + p2p.src.bytes() + p2p.off.bytes() + m2l.tgt.bytes() + m2l.src.bytes() + m2l.off.bytes();
   b += host_stage_q.bytes() + host_stage_phi.bytes() + host_stage_grad.bytes();
-  b += m2l_dmma.bytes();
+  b += m2l_dmma.bytes() + m2l4.bytes();
   b += shift_ops.bytes();
   b += let_dev.bytes();
   return b;
@@ -255,7 +257,8 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
     order_leaves_by_position(*P);
     choose_own_range(*P);
     const char* v = getenv("FMM_M2L_VARIANT");
-    if (v && v[0] >= '1' && v[0] <= '3') P->m2l_variant = v[0] - '0';
+    if (v && v[0] >= '1' && v[0] <= '4') P->m2l_variant = v[0] - '0';
+    if (P->m2l_variant == 4 && !fmm::m2l_v4_supported(p)) P->m2l_variant = 3;
     const char* nv = getenv("FMM_NEAR_VARIANT");
     if (nv && nv[0] == '1') P->near_variant = 1;
     const char* sv = getenv("FMM_SHIFT_VARIANT");
@@ -265,7 +268,10 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
     const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // test hook: export M2L-only local expansions
     P->debug_skip_l2l = dbg && dbg[0] == '1';
     if (dim == 3) {  // 3D translation operators (the 2D kernels are matrix-free)
-      if (P->m2l_variant >= 2) fmm::m2l_dmma_setup(*P);
+      if (P->m2l_variant == 4)
+        fmm::m2l_v4_setup(*P);
+      else if (P->m2l_variant >= 2)
+        fmm::m2l_dmma_setup(*P);
       fmm::shift_setup(*P);
     }
     P->M.alloc(P->cells.n * P->nc);
@@ -404,16 +410,16 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     b[FMM_B_PARTICLES] = P->keys.bytes() + P->perm.bytes() + P->pos.bytes() + P->host_stage_q.bytes() +
                          P->host_stage_phi.bytes() + P->host_stage_grad.bytes();
     b[FMM_B_TREE] = c.level.bytes() + c.begin.bytes() + c.end.bytes() + c.child.bytes() + c.nchild.bytes() +
-                    c.parent.bytes() + c.anchor.bytes() + c.center.bytes() + P->leaves.bytes();
+                    c.parent.bytes() + c.anchor.bytes() + c.center.bytes() + P->leaves.bytes() + P->m2l4.ihalf.bytes();
     b[FMM_B_LISTS] = P->p2p.tgt.bytes() + P->p2p.src.bytes() + P->p2p.off.bytes() + P->m2l.tgt.bytes() +
                      P->m2l.src.bytes() + P->m2l.off.bytes();
-    b[FMM_B_EXPANSIONS] = P->M.bytes() + P->L.bytes() + D.Mt.bytes();
+    b[FMM_B_EXPANSIONS] = P->M.bytes() + P->L.bytes() + D.Mt.bytes() + P->m2l4.Mt.bytes();
     b[FMM_B_OPERATORS] = D.ops.bytes() + D.rot_ops.bytes() + D.hpow.bytes() + D.symtab.bytes() +
                          D.rot_masks.bytes() + D.class_keys.bytes() + P->shift_ops.bytes();
     b[FMM_B_SCHEDULE] = D.col_src.bytes() + D.col_meta.bytes() + D.chunk_begin.bytes() + D.chunk_class.bytes() +
                         D.tile_chunk.bytes() + D.tile_cells.bytes() + D.chunk_seg.bytes() + D.seg_begin.bytes() +
                         D.rot_sched.bytes() + D.rot_ihdr.bytes() + D.rot_ipos.bytes() + D.rot_desc.bytes() +
-                        D.rot_order.bytes() + D.rot_scratch.bytes();
+                        D.rot_order.bytes() + D.rot_scratch.bytes() + P->m2l4.part.bytes();
     b[FMM_B_LET] = P->let_dev.bytes();
     int64_t s = 0;
     for (int k = 0; k < 7; ++k) s += b[k];
@@ -425,6 +431,11 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     if (P->dim == 2) {  // 2D log kernel: one complex multiply-add per (l, k) pair
       out->m2l_variant = 0;
       out->m2l_flops_per_pair = 8.0 * p1 * p1;
+    } else if (P->m2l_variant == 4) {  // per degree 2 (n^2+n+1) fixed-operator MACs + 2 zrot (4 n), twice;
+      double f = 0, z = 0;              // per order the Hankel (p+1-m)^2 (Re) + (Im, m > 0)
+      for (int n = 0; n <= P->p; ++n) f += 2.0 * (2.0 * (n * n + n + 1) + 4.0 * n);
+      for (int m = 0; m <= P->p; ++m) z += (m ? 2.0 : 1.0) * (p1 - m) * (p1 - m);
+      out->m2l_flops_per_pair = 2.0 * (f + z);
     } else if (P->m2l_variant == 3) {  // sum_n (n+1)^2 + n^2 per rotation stage, sum_m (p+1-m)^2 (Re) + (Im, m > 0)
       double rot = 0, z = 0;
       for (int n = 0; n <= P->p; ++n) rot += (n + 1.0) * (n + 1.0) + (double)n * n;
@@ -598,7 +609,9 @@ fmm_status fmm_let_finish(fmm_plan P, const double* shared_recv, const double* m
     P->near_fused_active = P->fuse_near && P->m2l_variant == 3 && P->near_variant == 2 && P->m2l_dmma.ntiles > 0;
     P->near_fused_grad = grad_send != nullptr;
     if (P->near_fused_active) fmm::near_fused_prepare(*P, grad_send != nullptr);
-    if (P->m2l_variant >= 2)
+    if (P->m2l_variant == 4)
+      fmm::m2l_v4_pass(*P);
+    else if (P->m2l_variant >= 2)
       fmm::m2l_dmma_pass(*P);
     else
       fmm::m2l_pass(*P);

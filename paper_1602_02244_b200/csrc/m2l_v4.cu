@@ -1,0 +1,746 @@
+// m2l_v4.cu — S9 M2L v4 (default for 2 <= p <= 12): the rotation ("point-and-shoot") form of
+// every M2L translation, one pair per lane, on the FP64 pipe (DFMA), with the only fixed
+// operator in constant memory.
+//
+// Paper: M2L dominates the FMM's run time (§2.2); "Rotating the multipole
+// expansion so that the translation is along the z-axis reduces the complexity from O(p^4)
+// to O(p^3)". This is the analytic, matrix-free end of the paper's
+// compute-memory axis: nothing per class is stored, every pair's operator is
+// formed on the fly from its own geometry.
+//
+// Factorisation (tools/proto_m2l_v4.py checks every step against the dense formula of
+// SURVEY §8(c) c.1, Lambda_j^k = sum_{n,m} (-1)^n M_n^m I_{j+n}^{k+m}(c_B - c_A)):
+//   d = c_B - c_A = rho (sin b cos a, sin b sin a, cos b),   Q = Ry(-b) Rz(-a),  Q d = rho z
+//   Lambda = A(Q)^T Z(rho) A(Q) M,   A(R) = action of rotation R on one degree's coefficients
+//   A(Ry(-b)) = A(P) A(Rz(-b)) A(P^-1),  P = Rx(-pi/2) fixed (Ry(t) = P Rz(t) P^-1)
+// In the real 2n+1 representation of a degree ([Re c0, Re c1, Im c1, Re c2, ...]):
+//   A(Rz(-t))        : (re, im) of order m -> e^{i m t} (re + i im)      ("zrot(t)", 4 flops)
+//   F  = A(P)        : fixed sparse real matrix, n^2 + n + 1 non-zeros (c_F4, host-computed)
+//   G  = A(P^-1)     : G_ik = (-1)^{m_i + m_k} F_ik  (P^-1 = Rz(pi) P Rz(pi))
+//   local side       : A(Q)^T = W^-1 zrot(a) F^T zrot(b) G^T W,  W = diag(1, 2, 2, ...)
+//   Z(rho)           : per order m the Hankel matrix (j+n)! / rho^{j+n+1} (z-axis translation)
+// so one pair is, per degree n:  zrot(a) -> G -> zrot(b) -> F  (multipole side),
+// per order m: Hankel (z translation), per degree j: G^T -> zrot(b) -> F^T -> zrot(a) (local
+// side), about 3.7K FP64 instructions at p = 10 — against 29K flops for the dense operator.
+// F's entries are the same for every pair, so they are constant-bank operands of the DFMAs
+// (uniform across the warp whatever the pairs; tools/cbank_probe.cu: ~32 TFLOP/s for a 4 KB
+// constant working set, p = 10 uses 3.6 KB).
+//
+// Scaled coefficients (as v2/v3): M~_n = (-1)^n M_n / h_B^n (the (-1)^n of the formula folded
+// in), Lambda~_j = Lambda_j h_A^{j+1}; distances in units of the target half side h_A, so the
+// Hankel entries are k!/u^{k+1} (u = rho / h_A) and the source side carries r^n, r = h_B / h_A
+// (an exact power of two).
+//
+// Kernel: one warp = one worker; lane = one pair. The pair list is grouped by target (S5);
+// "units" are kUnitChunks runs ("chunks") of 32 consecutive pairs, dealt round-robin to the warps
+// (every unit is the same work). Per chunk:
+//   1. the 32 source rows M~_B are copied into the warp's shared-memory buffer (one row per
+//      lane, coalesced 8-byte cp.async);
+//   2. each lane transforms its row IN PLACE (degree-major layout; stage 1 per degree, stage
+//      2 per order, stage 3 per degree): registers hold one degree or one order at a time;
+//   3. the warp sums the rows of lanes with the same target (segmented, in lane order) into
+//      per-lane running accumulators (lane k owns coefficients k, k+32, ...) — a target whose
+//      pairs continue into the next chunk keeps its accumulator; a finished target is
+//      written to L once. A target crossing a unit boundary leaves partial sums per unit, which a
+//      small fix-up kernel adds in unit order. Fixed order everywhere: bitwise deterministic, no
+//      atomics.
+#include <cmath>
+#include <algorithm>
+#include <complex>
+#include <utility>
+#include <vector>
+
+#include "plan.h"
+
+namespace fmm {
+namespace m2l4 {
+
+constexpr int kMinP = 2, kMaxP4 = 12;  // orders served by v4 (others: v3 / v2)
+constexpr int kUnitChunks = 16;        // default chunks of 32 pairs per work unit (balanced at launch)
+constexpr int kMaxWarpsPerCta = 8;     // M2L v4 CTA: up to 8 one-warp workers
+
+__host__ __device__ constexpr int nnzF(int n) { return n * n + n + 1; }
+__host__ __device__ constexpr int offF(int n) {
+  int s = 0;
+  for (int k = 0; k < n; ++k) s += nnzF(k);
+  return s;
+}
+constexpr int kFTotal = offF(kMaxP + 1);  // 1649 doubles (13 KB) for n = 0..16
+__host__ __device__ constexpr int ridx(int m, int part) { return m == 0 ? 0 : 2 * m - 1 + part; }
+
+// Does F_n have a (structurally) non-zero entry in row (m, pi), column (mp, pj)? Given the row
+// order m and the column order mp, there is at most one: F = Rz(-pi/2) d(-pi/2) Rz(pi/2) has
+// complex entries i^{m - mp} d_{m mp}(pi/2); folding m < 0 (real potential) keeps only Re
+// inputs when n + m is even and only Im inputs when n + m is odd, the output part follows the
+// parity of m - mp (+1 for Im inputs), and d_{m mp}(pi/2) vanishes for m = 0, n + mp odd and
+// for mp = 0, n + m odd. The host build below checks this pattern against the full matrix.
+__host__ __device__ constexpr bool f_entry(int n, int m, int mp, int& pi, int& pj) {
+  pj = ((n + m) & 1) ? 1 : 0;
+  if (mp == 0 && pj == 1) return false;
+  if (m == 0 && ((n + mp) & 1)) return false;
+  if (mp == 0 && ((n + m) & 1)) return false;
+  pi = ((m - mp + pj) & 1) ? 1 : 0;
+  if (m == 0 && pi == 1) return false;
+  return true;
+}
+constexpr int count_pattern(int n) {
+  int c = 0;
+  for (int m = 0; m <= n; ++m)
+    for (int mp = 0; mp <= n; ++mp) {
+      int pi = 0, pj = 0;
+      if (f_entry(n, m, mp, pi, pj)) ++c;
+    }
+  return c;
+}
+static_assert(count_pattern(0) == nnzF(0) && count_pattern(5) == nnzF(5) && count_pattern(10) == nnzF(10) &&
+                  count_pattern(16) == nnzF(16),
+              "F pattern count");
+
+}  // namespace m2l4
+
+namespace {
+using namespace m2l4;
+
+}  // namespace
+}  // namespace fmm
+// the fixed operator F (non-zeros of every degree), addressed by name from inline PTX
+extern "C" {
+__constant__ double fmm_c_F4[fmm::m2l4::kFTotal];
+}
+namespace fmm {
+namespace {
+using namespace m2l4;
+
+// ------------------------------------------------------------------ host: the fixed operator
+using cld = std::complex<long double>;
+
+// R_n^m(x) for m >= 0, n <= p (Cartesian recurrences of SURVEY §8(c) c.1), long double
+void host_regular(long double x, long double y, long double z, int p, std::vector<cld>& R) {
+  R.assign((p + 1) * (p + 2) / 2, cld(0));
+  const long double r2 = x * x + y * y + z * z;
+  cld d(1);
+  for (int m = 0; m <= p; ++m) {
+    if (m > 0) d = d * cld(-x / (2 * m), -y / (2 * m));
+    R[cidx(m, m)] = d;
+    if (m + 1 > p) continue;
+    cld a = d, b = d * z;
+    R[cidx(m + 1, m)] = b;
+    for (int n = m + 2; n <= p; ++n) {
+      const cld c = ((long double)(2 * n - 1) * z * b - r2 * a) / (long double)((n + m) * (n - m));
+      R[cidx(n, m)] = c;
+      a = b;
+      b = c;
+    }
+  }
+}
+cld host_Rget(const std::vector<cld>& R, int n, int m) {
+  if (m >= 0) return R[cidx(n, m)];
+  const cld v = std::conj(R[cidx(n, -m)]);
+  return (m & 1) ? -v : v;
+}
+
+// Gauss-Legendre nodes / weights on [-1, 1] (Newton on P_K), long double
+void gauss_legendre(int K, std::vector<long double>& t, std::vector<long double>& w) {
+  t.resize(K);
+  w.resize(K);
+  const long double pi = 3.14159265358979323846264338327950288L;
+  for (int i = 0; i < K; ++i) {
+    long double x = std::cos(pi * (i + 0.75L) / (K + 0.5L)), dp = 0;
+    for (int it = 0; it < 100; ++it) {
+      long double p0 = 1, p1 = x;
+      for (int k = 2; k <= K; ++k) {
+        const long double p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = K * (x * p1 - p0) / (x * x - 1);
+      const long double dx = p1 / dp;
+      x -= dx;
+      if (std::fabs(dx) < 1e-19L) break;
+    }
+    t[i] = x;
+    w[i] = 2 / ((1 - x * x) * dp * dp);
+  }
+}
+
+// Real (2n+1)^2 matrices of A(Rx(sgn * pi/2)) for n = 0..kMaxP, by exact sphere quadrature:
+// A_{m m'} = (2n+1)(n+m')!(n-m')!/(4 pi) * integral conj R_n^m(Rx x) R_n^m'(x) dOmega
+// (orthogonality of the harmonics), then folded to the real representation.
+std::vector<std::vector<double>> rotation_real(int sgn) {
+  const int p = kMaxP, K = p + 2, L = 2 * p + 4;
+  std::vector<long double> gt, gw;
+  gauss_legendre(K, gt, gw);
+  const long double pi = 3.14159265358979323846264338327950288L;
+  // complex A[n][(m+n)*(2n+1) + (m'+n)]
+  std::vector<std::vector<cld>> A(p + 1);
+  for (int n = 0; n <= p; ++n) A[n].assign((2 * n + 1) * (2 * n + 1), cld(0));
+  std::vector<cld> R0, R1;
+  for (int i = 0; i < K; ++i)
+    for (int l = 0; l < L; ++l) {
+      const long double st = std::sqrt(1 - gt[i] * gt[i]), ph = 2 * pi * l / L;
+      const long double x = st * std::cos(ph), y = st * std::sin(ph), z = gt[i];
+      const long double wq = gw[i] * 2 * pi / L;
+      host_regular(x, y, z, p, R0);
+      // Rx(-pi/2): (x, y, z) -> (x, z, -y); Rx(+pi/2): (x, y, z) -> (x, -z, y)
+      if (sgn < 0)
+        host_regular(x, z, -y, p, R1);
+      else
+        host_regular(x, -z, y, p, R1);
+      for (int n = 0; n <= p; ++n)
+        for (int m = -n; m <= n; ++m) {
+          const cld a = std::conj(host_Rget(R1, n, m)) * wq;
+          for (int mp = -n; mp <= n; ++mp) A[n][(m + n) * (2 * n + 1) + (mp + n)] += a * host_Rget(R0, n, mp);
+        }
+    }
+  std::vector<std::vector<double>> F(p + 1);
+  for (int n = 0; n <= p; ++n) {
+    const int D = 2 * n + 1;
+    for (int mp = -n; mp <= n; ++mp) {
+      long double f = (2 * n + 1) / (4 * pi);
+      for (int k = 2; k <= n + mp; ++k) f *= k;
+      for (int k = 2; k <= n - mp; ++k) f *= k;
+      for (int m = -n; m <= n; ++m) A[n][(m + n) * D + (mp + n)] *= f;
+    }
+    F[n].assign(D * D, 0.0);
+    for (int k = 0; k < D; ++k) {  // column k: basis vector e_k of the real representation
+      const int mk = (k + 1) / 2, pk = k == 0 ? 0 : ((k + 1) & 1);
+      std::vector<cld> c(D, cld(0));
+      const cld v = pk ? cld(0, 1) : cld(1, 0);
+      c[n + mk] = v;
+      if (mk > 0) c[n - mk] = (mk & 1) ? -std::conj(v) : std::conj(v);
+      for (int m = 0; m <= n; ++m) {
+        cld o(0);
+        for (int mp = -n; mp <= n; ++mp) o += A[n][(m + n) * D + (mp + n)] * c[mp + n];
+        F[n][ridx(m, 0) * D + k] = (double)o.real();
+        if (m > 0) F[n][ridx(m, 1) * D + k] = (double)o.imag();
+      }
+    }
+  }
+  return F;
+}
+
+// Packed non-zeros of F in the kernels' enumeration order (m, mp), after checking the pattern
+// and the sign relation G = (-1)^{m + m'} F against the separately computed A(P^-1).
+std::vector<double> build_f_table() {
+  const auto F = rotation_real(-1), G = rotation_real(+1);
+  std::vector<double> out;
+  out.reserve(kFTotal);
+  for (int n = 0; n <= kMaxP; ++n) {
+    const int D = 2 * n + 1;
+    double mx = 0;
+    for (double v : F[n]) mx = std::fmax(mx, std::fabs(v));
+    std::vector<char> used(D * D, 0);
+    for (int m = 0; m <= n; ++m)
+      for (int mp = 0; mp <= n; ++mp) {
+        int pi = 0, pj = 0;
+        if (!f_entry(n, m, mp, pi, pj)) continue;
+        const int r = ridx(m, pi), k = ridx(mp, pj);
+        out.push_back(F[n][r * D + k]);
+        used[r * D + k] = 1;
+      }
+    for (int r = 0; r < D; ++r)
+      for (int k = 0; k < D; ++k) {
+        const int mr = (r + 1) / 2, mk = (k + 1) / 2;
+        const double g = ((mr + mk) & 1) ? -F[n][r * D + k] : F[n][r * D + k];
+        if (std::fabs(G[n][r * D + k] - g) > 1e-13 * mx)
+          throw Error(FMM_ERR_NUMERIC, "m2l v4: A(P^-1) != sign-flipped A(P) (internal)");
+        if (!used[r * D + k] && std::fabs(F[n][r * D + k]) > 1e-13 * mx)
+          throw Error(FMM_ERR_NUMERIC, "m2l v4: rotation pattern mismatch (internal)");
+      }
+  }
+  if ((int)out.size() != kFTotal) throw Error(FMM_ERR_NUMERIC, "m2l v4: table size (internal)");
+  return out;
+}
+
+// ------------------------------------------------------------------ device: one pair's stages
+// F_N's non-zeros in enumeration order (compile time): output index r, input index k, G's sign
+struct FEnt {
+  int r, k, mrow, prow, mcol, pcol;
+  bool gneg;
+};
+template <int N>
+struct FTab {
+  FEnt e[nnzF(N)];
+};
+template <int N>
+constexpr FTab<N> make_ftab() {
+  FTab<N> t{};
+  int i = 0;
+  for (int m = 0; m <= N; ++m)
+    for (int mp = 0; mp <= N; ++mp) {
+      int pi = 0, pj = 0;
+      if (!f_entry(N, m, mp, pi, pj)) continue;
+      t.e[i++] = FEnt{ridx(m, pi), ridx(mp, pj), m, pi, mp, pj, ((m + mp) & 1) != 0};
+    }
+  return t;
+}
+template <int N>
+struct FTabOf {
+  static constexpr FTab<N> value = make_ftab<N>();
+};
+
+// sign of a stage-3 input element (Re of order m: (-1)^m, Im: -(-1)^m: the Hankel output's sign)
+__host__ __device__ constexpr bool sx_neg(int m, int part) { return part == 0 ? (m & 1) : !(m & 1); }
+
+// y += F x (T: y += F^T x); SG: G's signs (-1)^{m + mp}; SX: stage-3 input signs
+template <int N, bool T, bool SG, bool SX, int I>
+__device__ __forceinline__ void fstep(const double (&x)[2 * N + 1], double (&y)[2 * N + 1], int z) {
+  constexpr FEnt E = FTabOf<N>::value.e[I];
+  constexpr bool neg = (SG && E.gneg) != (SX && (T ? sx_neg(E.mrow, E.prow) : sx_neg(E.mcol, E.pcol)));
+  const double f = fmm_c_F4[offF(N) + I + 2 * z];  // (2 z: 16-byte aligned, LDCU.128 pairs)
+  const double c = neg ? -f : f;
+  if constexpr (!T)
+    y[E.r] = fma(c, x[E.k], y[E.r]);
+  else
+    y[E.k] = fma(c, x[E.r], y[E.k]);
+}
+template <int N, bool T, bool SG, bool SX, int... I>
+__device__ __forceinline__ void apply_seq(const double (&x)[2 * N + 1], double (&y)[2 * N + 1],
+                                          int z, std::integer_sequence<int, I...>) {
+  (fstep<N, T, SG, SX, I>(x, y, z), ...);
+}
+// z: a run-time zero the compiler cannot see (zmask = 0), different per call site and per chunk
+// and warp-uniform: the constants are loaded (LDCU, uniform datapath) right where they are used,
+// never held in registers across pairs or shared between the stages
+template <int N, bool T, bool SG, bool SX>
+__device__ __forceinline__ void apply_fixed(const double (&x)[2 * N + 1], double (&y)[2 * N + 1], int z) {
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) y[i] = 0.0;
+  apply_seq<N, T, SG, SX>(x, y, z, std::make_integer_sequence<int, nnzF(N)>{});
+}
+
+// (re, im) of order m -> e^{i m t} (re + i im), m = 1..N; cs[m] = (cos mt, sin mt)
+template <int N>
+__device__ __forceinline__ void zrot(double (&x)[2 * N + 1], const double2* cs) {
+#pragma unroll
+  for (int m = 1; m <= N; ++m) {
+    const double re = x[2 * m - 1], im = x[2 * m];
+    x[2 * m - 1] = fma(cs[m].x, re, -cs[m].y * im);
+    x[2 * m] = fma(cs[m].y, re, cs[m].x * im);
+  }
+}
+
+// stage 1 (multipole side) of degree N, in place in the lane's row w (degree-major)
+template <int N>
+__device__ __forceinline__ void stage1(double* w, double rn, const double2* ca, const double2* cb, int z0, int z1) {
+  double x[2 * N + 1], t[2 * N + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) x[i] = w[N * N + i] * rn;
+  zrot<N>(x, ca);
+  apply_fixed<N, false, true, false>(x, t, z0);
+  zrot<N>(t, cb);
+  apply_fixed<N, false, false, false>(t, x, z1);
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) w[N * N + i] = x[i];
+}
+
+// stage 2: z-axis translation of order M, part PART (Hankel h[j + n]); m = 0 rows halved
+// (the W / V bookkeeping of the local side: V = diag(2, 1, ...), A(Q)^T = V X V^-1)
+template <int P, int M, int PART>
+__device__ __forceinline__ void stage2(double* w, const double* h) {
+  constexpr int L = P + 1 - M;
+  double a[L], y[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) a[i] = w[(M + i) * (M + i) + ridx(M, PART)];
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int n = 0; n < L; ++n) s = fma(h[2 * M + j + n], a[n], s);
+    y[j] = M == 0 ? 0.5 * s : s;
+  }
+#pragma unroll
+  for (int i = 0; i < L; ++i) w[(M + i) * (M + i) + ridx(M, PART)] = y[i];
+}
+
+// stage 3 (local side) of degree N, in place
+template <int N>
+__device__ __forceinline__ void stage3(double* w, const double2* ca, const double2* cb, int z0, int z1) {
+  double x[2 * N + 1], t[2 * N + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) x[i] = w[N * N + i];
+  apply_fixed<N, true, true, true>(x, t, z0);
+  zrot<N>(t, cb);
+  apply_fixed<N, true, false, false>(t, x, z1);
+  zrot<N>(x, ca);
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) w[N * N + i] = x[i];
+}
+
+// (the empty asm with a memory clobber keeps the compiler from hoisting the next degree's
+// shared-memory loads above this degree's stores: one degree / order live at a time)
+__device__ __forceinline__ void order_fence() { asm volatile("" ::: "memory"); }
+
+template <int P, int N = 0>
+__device__ __forceinline__ void stage1_all(double* w, double r, double rn, const double2* ca, const double2* cb,
+                                           const int (&z)[4]) {
+  stage1<N>(w, rn, ca, cb, z[0], z[1]);
+  order_fence();
+  if constexpr (N < P) stage1_all<P, N + 1>(w, r, rn * r, ca, cb, z);
+}
+template <int P, int M = 0>
+__device__ __forceinline__ void stage2_all(double* w, const double* h) {
+  stage2<P, M, 0>(w, h);
+  order_fence();
+  if constexpr (M > 0) stage2<P, M, 1>(w, h);
+  order_fence();
+  if constexpr (M < P) stage2_all<P, M + 1>(w, h);
+}
+template <int P, int N = 0>
+__device__ __forceinline__ void stage3_all(double* w, const double2* ca, const double2* cb, const int (&z)[4]) {
+  stage3<N>(w, ca, cb, z[2], z[3]);
+  order_fence();
+  if constexpr (N < P) stage3_all<P, N + 1>(w, ca, cb, z);
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// 1/sqrt(x) to full double precision: MUFU seed (rsqrt.approx.ftz.f64, ~2^-20; x is a squared
+// distance >= 1 in target half sides, never subnormal), a Newton step and a third-order step
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-x * y, y, 1.0);
+  return fma(y, fma(0.375, e, 0.5) * e, y);
+}
+
+struct V4Args {
+  const int32_t* tgt;      // [npairs] grouped by target
+  const int32_t* src;
+  int64_t npairs, nunits;  // units: uchunks chunks of 32 pairs of the flat list
+  int uchunks;
+ const double4* center;   // cells: x, y, z, h
+  const double* ihalf;     // [ncells] 1 / h
+  const int32_t* level;
+  const double* Mt;        // [ncells][NR] (-1)^n M_n / h^n, degree-major real
+  double2* L;              // [ncells][nc]
+  double* part;            // [nunits][2][NR] partial sums of targets crossing unit boundaries
+  int zmask;               // 0 (see apply_fixed)
+};
+
+template <int P>
+struct V4Geo {
+  static constexpr int NR = (P + 1) * (P + 1);
+  static constexpr int NRS = NR | 1;  // odd row stride: lane-private 8-byte accesses conflict-free
+  static constexpr int KPL = (NR + 31) / 32;
+};
+
+// Lambda = V Lambda~ / h^{j+1} (V: m = 0 entries x 2) of target t from the per-lane sums (lane k
+// owns real coefficients q = k + 32 c), into the complex (n, m >= 0) layout of L
+template <int P>
+__device__ __forceinline__ void write_target(const V4Args& a, int t, const double (&acc)[V4Geo<P>::KPL], int lane) {
+  constexpr int NR = V4Geo<P>::NR;
+  const double ih = a.ihalf[t];
+  double* Lc = (double*)(a.L + (int64_t)t * ((P + 1) * (P + 2) / 2));
+#pragma unroll
+  for (int c = 0; c < V4Geo<P>::KPL; ++c) {
+    const int q = lane + 32 * c;
+    if (q >= NR) continue;
+    int j = 0;
+    while ((j + 1) * (j + 1) <= q) ++j;
+    const int r = q - j * j, m = (r + 1) >> 1, part = r > 0 ? ((r + 1) & 1) : 0;
+    double s = m == 0 ? 2.0 * ih : ih;
+    for (int k = 0; k < j; ++k) s *= ih;
+    Lc[2 * cidx(j, m) + part] = acc[c] * s;
+  }
+}
+
+// a finished segment of target t in unit u: written to L if the target lies inside the unit,
+// else its partial sum goes to part[u][0] (target began in an earlier unit) or part[u][1]
+template <int P>
+__device__ __forceinline__ void finish_segment(const V4Args& a, int64_t u, int t, bool from_prev, bool to_next,
+                                            const double (&acc)[V4Geo<P>::KPL], int lane) {
+  constexpr int NR = V4Geo<P>::NR;
+  if (!from_prev && !to_next) {
+    write_target<P>(a, t, acc, lane);
+    return;
+  }
+  double* d = a.part + (u * 2 + (from_prev ? 0 : 1)) * NR;
+#pragma unroll
+  for (int c = 0; c < V4Geo<P>::KPL; ++c)
+    if (lane + 32 * c < NR) d[lane + 32 * c] = acc[c];
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V4Args a) {
+  using G = V4Geo<P>;
+  constexpr int NR = G::NR, NRS = G::NRS, KPL = G::KPL;
+  const int64_t UP = 32 * (int64_t)a.uchunks;
+  extern __shared__ double sm4[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* const wb = sm4 + (size_t)warp * 32 * NRS;
+  double* const w = wb + lane * NRS;
+  // static round-robin over equal-work units; every warp of the CTA runs the same number of
+  // units and chunks (a barrier after each stage keeps the warps on the same instructions:
+  // the unrolled code is larger than the instruction cache, so warps in step share its fetches)
+  const int64_t per_round = (int64_t)gridDim.x * nw;
+  const int rounds = (int)((a.nunits + per_round - 1) / per_round);
+  for (int it = 0; it < rounds; ++it) {
+    const int64_t u = ((int64_t)it * gridDim.x + blockIdx.x) * nw + warp;  // may be >= nunits: idle
+    const int64_t u0 = min(u * UP, a.npairs), u1 = min(u0 + UP, a.npairs);
+    const int tprev = u0 > 0 && u0 < a.npairs ? a.tgt[u0 - 1] : -1;  // target continued from the previous unit
+    const int tnext = u1 < a.npairs ? a.tgt[u1] : -1;               // target continued in the next unit
+    int cur = -1;
+    double acc[KPL];
+#pragma unroll
+    for (int c = 0; c < KPL; ++c) acc[c] = 0.0;
+    for (int ich = 0; ich < a.uchunks; ++ich) {
+      const int64_t base = u0 + 32 * ich;
+      const int nact = (int)max((int64_t)0, min((int64_t)32, u1 - base));
+      const bool act = lane < nact;
+      const int tg = act ? a.tgt[base + lane] : -1;
+      const int sr = act ? a.src[base + lane] : 0;
+      // 1. source rows into the lanes' buffers (coalesced: row by row)
+      for (int l = 0; l < nact; ++l) {
+        const int s = __shfl_sync(0xffffffffu, sr, l);
+        const double* g = a.Mt + (int64_t)s * NR;
+#pragma unroll
+        for (int c = 0; c < KPL; ++c) {
+          const int q = lane + 32 * c;
+          if (q < NR) cp_async8(wb + l * NRS + q, g + q);
+        }
+      }
+      // geometry of the lane's pair (overlaps the copies)
+      // (inactive lanes of a ragged chunk run the same code on the chunk's first pair and their
+      // own stale rows — no divergence, results unused: the stages stay warp-uniform)
+      double2 ca[P + 1], cb[P + 1], e1, e2;
+      double r = 1.0, iu = 0.0;
+      // (no IEEE division or sqrt here: their slow-path subroutine calls would force every
+      // loop-carried value out of the uniform registers; rsqrt is inline)
+      {
+        int tgi = __shfl_sync(0xffffffffu, tg, act ? lane : 0), sri = __shfl_sync(0xffffffffu, sr, act ? lane : 0);
+        if (nact == 0) tgi = sri = 0;  // idle chunk: any valid cell (results unused)
+        const double4 A = a.center[tgi], B = a.center[sri];
+        const double ih = a.ihalf[tgi];
+        const double dx = (B.x - A.x) * ih, dy = (B.y - A.y) * ih, dz = (B.z - A.z) * ih;
+        const double rxy2 = dx * dx + dy * dy, u2 = rxy2 + dz * dz;
+        iu = rsqrt_nr(u2);
+        if (rxy2 > 0.0) {
+          const double ir = rsqrt_nr(rxy2);
+          e1 = make_double2(dx * ir, dy * ir);
+          e2 = make_double2(dz * iu, rxy2 * ir * iu);
+        } else {
+          e1 = make_double2(1.0, 0.0);
+          e2 = make_double2(dz * iu, 0.0);
+        }
+        r = __hiloint2double((1023 + a.level[tgi] - a.level[sri]) << 20, 0);  // h_B / h_A = 2^{l_A - l_B}
+      }
+      ca[0] = cb[0] = make_double2(1.0, 0.0);
+      ca[1] = e1;
+      cb[1] = e2;
+#pragma unroll
+      for (int m = 2; m <= P; ++m) {
+        ca[m] = make_double2(fma(ca[m - 1].x, e1.x, -ca[m - 1].y * e1.y), fma(ca[m - 1].x, e1.y, ca[m - 1].y * e1.x));
+        cb[m] = make_double2(fma(cb[m - 1].x, e2.x, -cb[m - 1].y * e2.y), fma(cb[m - 1].x, e2.y, cb[m - 1].y * e2.x));
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      // 2. the pair's rotation-translation-rotation, in place
+      {
+        int z[4];
+        int zc;
+        asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(zc));  // re-read per chunk: uniform (S2UR), opaque
+#pragma unroll
+        for (int k = 0; k < 4; ++k) z[k] = (zc * (k + 1)) & a.zmask;
+        stage1_all<P>(w, r, 1.0, ca, cb, z);
+        __syncthreads();
+        double h[2 * P + 1];  // Hankel entries k! / u^{k+1}
+        h[0] = iu;
+#pragma unroll
+        for (int k = 1; k <= 2 * P; ++k) h[k] = h[k - 1] * (k * iu);
+        stage2_all<P>(w, h);
+        __syncthreads();
+        stage3_all<P>(w, ca, cb, z);
+      }
+      __syncwarp();
+      // 3. segmented sum over lanes with the same target (lane order)
+      for (int l = 0; l < nact; ++l) {
+        const int t = __shfl_sync(0xffffffffu, tg, l);
+        if (t != cur) {
+          if (cur >= 0) finish_segment<P>(a, u, cur, cur == tprev, false, acc, lane);
+          cur = t;
+#pragma unroll
+          for (int c = 0; c < KPL; ++c) acc[c] = 0.0;
+        }
+        const double* row = wb + l * NRS;
+#pragma unroll
+        for (int c = 0; c < KPL; ++c)
+          if (lane + 32 * c < NR) acc[c] += row[lane + 32 * c];
+      }
+      __syncthreads();
+    }
+    if (cur >= 0) finish_segment<P>(a, u, cur, cur == tprev, cur == tnext, acc, lane);
+  }
+}
+
+// Targets crossing unit boundaries: one warp per unit whose last target continues into the next
+// unit and began in this one; partial sums added in unit order (deterministic), then written.
+template <int P>
+__global__ void m2l_v4_fixup_kernel(const V4Args a) {
+  using G = V4Geo<P>;
+  constexpr int NR = G::NR, KPL = G::KPL;
+  const int64_t UP = 32 * (int64_t)a.uchunks;
+  const int lane = threadIdx.x & 31;
+  const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (u >= a.nunits) return;
+  const int64_t u0 = u * UP, u1 = min(u0 + UP, a.npairs);
+  if (u1 >= a.npairs) return;
+  const int t = a.tgt[u1 - 1];
+  if (a.tgt[u1] != t) return;                 // last target ends inside this unit
+  if (u0 > 0 && a.tgt[u0 - 1] == t) return;   // began in an earlier unit: handled there
+  double acc[KPL];
+#pragma unroll
+  for (int c = 0; c < KPL; ++c) acc[c] = lane + 32 * c < NR ? a.part[(u * 2 + 1) * NR + lane + 32 * c] : 0.0;
+  for (int64_t v = u + 1; v < a.nunits; ++v) {
+#pragma unroll
+    for (int c = 0; c < KPL; ++c)
+      if (lane + 32 * c < NR) acc[c] += a.part[(v * 2) * NR + lane + 32 * c];
+    const int64_t v1 = min((v + 1) * UP, a.npairs);
+    if (v1 >= a.npairs || a.tgt[v1] != t) break;  // t ends in unit v
+  }
+  write_target<P>(a, t, acc, lane);
+}
+
+// M~[c][q] = (-1)^n {Re, Im} M_n^m(c) / h_c^n, degree-major real layout q = n^2 + ridx(m, part)
+__global__ void m2l4_mtilde_kernel(const double2* __restrict__ M, const double4* __restrict__ center, int64_t ncells,
+                                   int p, int nc, int NR, double* __restrict__ Mt, double* __restrict__ ihalf) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncells * NR) return;
+  const int64_t c = i / NR;
+  const int q = (int)(i - c * NR);
+  if (q == 0) ihalf[c] = 1.0 / center[c].w;
+  int n = 0;
+  while ((n + 1) * (n + 1) <= q) ++n;
+  const int t = q - n * n, m = (t + 1) >> 1, part = t > 0 ? ((t + 1) & 1) : 0;
+  const double2 v = M[c * nc + cidx(n, m)];
+  const double ih = 1.0 / center[c].w;
+  double s = (n & 1) ? -1.0 : 1.0;
+  for (int k = 0; k < n; ++k) s *= ih;
+  Mt[i] = (part ? v.y : v.x) * s;
+}
+
+// launch geometry (setup): warps per CTA from shared memory and registers, units sized so every
+// warp gets the same number of units (as close to kUnitChunks chunks as that allows)
+template <int P>
+void size_v4(fmm_plan_s& P_) {
+  using G = V4Geo<P>;
+  M2L4& V = P_.m2l4;
+  const size_t sh = (size_t)32 * G::NRS * sizeof(double);
+  FMM_CUDA(cudaFuncSetAttribute(m2l_v4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  int nsm = 148;
+  FMM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P_.device));
+  cudaFuncAttributes fa;
+  FMM_CUDA(cudaFuncGetAttributes(&fa, m2l_v4_kernel<P>));
+  const int by_smem = (int)((227 * 1024) / sh), by_regs = 65536 / (32 * std::max(1, fa.numRegs));
+  const int fit = std::max(1, std::min({by_smem, by_regs, kMaxWarpsPerCta}));
+  V.wpc = std::max(1, std::min(V.warps_per_sm > 0 ? V.warps_per_sm : fit, fit));
+  V.smem = sh * V.wpc;
+  const int64_t nchunks = (P_.m2l.n + 31) / 32, warps = (int64_t)nsm * V.wpc;
+  V.uchunks = V.unit_chunks;
+  if (V.uchunks <= 0) {
+    const int64_t rounds = std::max<int64_t>(1, (nchunks + warps * kUnitChunks - 1) / (warps * kUnitChunks));
+    V.uchunks = (int)std::max<int64_t>(1, (nchunks + rounds * warps - 1) / (rounds * warps));
+  }
+  V.nunits = (nchunks + V.uchunks - 1) / V.uchunks;
+  V.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nsm, (V.nunits + V.wpc - 1) / V.wpc));
+  V.part.alloc(V.nunits * 2 * G::NR);
+}
+
+template <int P>
+void launch_v4(fmm_plan_s& P_, const V4Args& a) {
+  const M2L4& V = P_.m2l4;
+  m2l_v4_kernel<P><<<(unsigned)V.grid, 32 * V.wpc, V.smem, P_.stream>>>(a);
+  FMM_LAUNCHED("m2l_v4_kernel");
+  if (a.nunits > 1) {
+    m2l_v4_fixup_kernel<P><<<cdiv(a.nunits, 4), 128, 0, P_.stream>>>(a);
+    FMM_LAUNCHED("m2l_v4_fixup_kernel");
+  }
+}
+
+template <int P>
+void dispatch_v4(fmm_plan_s& P_, const V4Args* a) {  // a == nullptr: size at setup
+  if (a)
+    launch_v4<P>(P_, *a);
+  else
+    size_v4<P>(P_);
+}
+
+void v4_switch(fmm_plan_s& P, const V4Args* a) {
+  switch (P.p) {
+#ifdef FMM_V4_ONLY  // development builds: one instantiation (compile time)
+    case FMM_V4_ONLY: dispatch_v4<FMM_V4_ONLY>(P, a); break;
+#else
+    case 2: dispatch_v4<2>(P, a); break;
+    case 3: dispatch_v4<3>(P, a); break;
+    case 4: dispatch_v4<4>(P, a); break;
+    case 5: dispatch_v4<5>(P, a); break;
+    case 6: dispatch_v4<6>(P, a); break;
+    case 7: dispatch_v4<7>(P, a); break;
+    case 8: dispatch_v4<8>(P, a); break;
+    case 9: dispatch_v4<9>(P, a); break;
+    case 10: dispatch_v4<10>(P, a); break;
+    case 11: dispatch_v4<11>(P, a); break;
+    case 12: dispatch_v4<12>(P, a); break;
+#endif
+    default: throw Error(FMM_ERR_USAGE, "m2l v4: order out of range");
+  }
+}
+
+}  // namespace
+
+bool m2l_v4_supported(int p) { return p >= kMinP && p <= kMaxP4; }
+
+void m2l_v4_setup(fmm_plan_s& P) {
+  static std::vector<double> table;  // host copy (same for every plan)
+  static bool built = false;
+  if (!built) {
+    table = build_f_table();
+    built = true;
+  }
+  FMM_CUDA(cudaMemcpyToSymbolAsync(fmm_c_F4, table.data(), sizeof(double) * kFTotal, 0, cudaMemcpyHostToDevice,
+                                   P.stream));
+  M2L4& V = P.m2l4;
+  const int NR = (P.p + 1) * (P.p + 1);
+  V.Mt.alloc(P.cells.n * NR);
+  V.ihalf.alloc(P.cells.n);
+  const char* w = getenv("FMM_V4_WARPS");
+  V.warps_per_sm = w ? atoi(w) : 0;
+  const char* uc = getenv("FMM_V4_UNIT_CHUNKS");  // tests: small units cross many targets
+  V.unit_chunks = uc ? atoi(uc) : 0;
+  V.nunits = 0;
+  if (P.m2l.n > 0) v4_switch(P, nullptr);
+  FMM_CUDA(cudaStreamSynchronize(P.stream));
+}
+
+void m2l_v4_pass(fmm_plan_s& P) {
+  M2L4& V = P.m2l4;
+  FMM_CUDA(cudaMemsetAsync(P.L.ptr, 0, sizeof(double2) * P.L.count, P.stream));
+  if (V.nunits == 0) return;
+  const int NR = (P.p + 1) * (P.p + 1);
+  const int64_t ne = P.cells.n * NR;
+  m2l4_mtilde_kernel<<<cdiv(ne, 256), 256, 0, P.stream>>>(P.M, P.cells.center, P.cells.n, P.p, P.nc, NR, V.Mt,
+                                                           V.ihalf);
+  FMM_LAUNCHED("m2l4_mtilde_kernel");
+  V4Args a;
+  a.tgt = P.m2l.tgt;
+  a.src = P.m2l.src;
+  a.npairs = P.m2l.n;
+  a.nunits = V.nunits;
+  a.uchunks = V.uchunks;
+  a.center = P.cells.center;
+  a.ihalf = V.ihalf;
+  a.level = P.cells.level;
+  a.Mt = V.Mt;
+  a.L = P.L;
+  a.part = V.part;
+  a.zmask = 0;
+  v4_switch(P, &a);
+}
+
+}  // namespace fmm

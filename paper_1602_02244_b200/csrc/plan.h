@@ -104,6 +104,19 @@ struct M2LDmma {
   }
 };
 
+// M2L v4 state (m2l_v4.cu): work units over the target-grouped pair list, scaled multipoles
+struct M2L4 {
+  DevBuf<double> Mt;        // [ncells][(p+1)^2] (-1)^n M_n / h^n, degree-major real layout
+  DevBuf<double> part;      // [nunits][2][(p+1)^2] partial sums of targets crossing unit boundaries
+  DevBuf<double> ihalf;     // [ncells] inverse half sides
+  int64_t nunits = 0;       // > 0 if there are M2L pairs (units of chunks of 32 pairs, sized at launch)
+  int warps_per_sm = 0;     // 0 = as many as shared memory / registers allow (FMM_V4_WARPS)
+  int unit_chunks = 0;      // 0 = balanced at setup (FMM_V4_UNIT_CHUNKS: tests)
+  int uchunks = 0, wpc = 1, grid = 1;  // launch geometry (setup)
+  size_t smem = 0;
+  int64_t bytes() const { return Mt.bytes() + part.bytes() + ihalf.bytes(); }
+};
+
 // LET exchange lists of one rank (let.cu); counts per peer rank, index lists concatenated in rank order.
 struct LetLists {
   int world = 1;
@@ -162,8 +175,11 @@ struct fmm_plan_s {
   fmm::PairList p2p, m2l;
   int64_t n_p2p_interactions = 0;
   fmm::M2LDmma m2l_dmma;
-  int m2l_variant = 3;  // 1 = matrix-free O(p^4) per pair (v1), 2 = dense DMMA operator classes (v2),
-                        // 3 = rotation-factored DMMA operator classes (v3, p <= 14; else v2)
+  fmm::M2L4 m2l4;
+  int m2l_variant = 4;  // 1 = matrix-free O(p^4) per pair (v1), 2 = dense DMMA operator classes (v2),
+                        // 3 = rotation-factored DMMA operator classes (v3, p <= 14; else v2),
+                        // 4 = per-pair rotation on DFMA with a fixed constant-bank operator
+                        //     (2 <= p <= 12; else v3)
   int near_variant = 2; // 1 = block per leaf, thread per target (v1), 2 = warp per leaf (v2)
 
   // this rank's targets (Morton range of sorted positions) and its leaves
@@ -217,6 +233,9 @@ void m2l_pass(fmm_plan_s& P);
 void m2l_dmma_setup(fmm_plan_s& P);
 void m2l_dmma_pass(fmm_plan_s& P);
 bool m2l_rot_supported(int p);
+bool m2l_v4_supported(int p);
+void m2l_v4_setup(fmm_plan_s& P);
+void m2l_v4_pass(fmm_plan_s& P);
 void m2l_rot_setup(fmm_plan_s& P);
 size_t rot_smem_bytes(int p, int T, int smax);
 int rot_chunk_width(int p);

@@ -241,16 +241,18 @@ def test_full_size_sampled_parity(torch_cuda, name, k):
     assert O.rel_l2(phi[T][:200], pd) < 1e-4  # truncation-level agreement with direct
 
 
-@pytest.mark.parametrize("variant", ["1", "2", "3"])
+@pytest.mark.parametrize("variant", ["1", "2", "3", "4"])
 @pytest.mark.parametrize("dist,n,p,ncrit,theta", [("plummer", 20000, 6, 32, 0.5), ("plummer", 5000, 1, 7, 0.3),
                                                   ("sphere", 20000, 5, 40, 0.35), ("cube", 20000, 14, 64, 0.4),
                                                   ("plummer", 20000, 9, 40, 0.5), ("sphere", 20000, 12, 128, 0.4),
                                                   ("cube", 20000, 2, 32, 0.5), ("sphere", 20000, 3, 40, 0.4),
                                                   ("plummer", 20000, 4, 16, 0.5), ("cube", 8000, 0, 16, 0.5)])
 def test_m2l_variants(torch_cuda, monkeypatch, variant, dist, n, p, ncrit, theta):
-    """The three M2L formulations — v1 matrix-free O(p^4) per pair (the paper's analytic end),
-    v2 precomputed dense translation-invariant operators on DMMA and v3 the
-    same operators rotation-factored (p <= 14, else v2) — match the oracle."""
+    """The four M2L formulations — v1 matrix-free O(p^4) per pair (the paper's analytic end),
+    v2 precomputed dense translation-invariant operators on DMMA, v3 the
+    same operators rotation-factored (p <= 14, else v2) and v4 the per-pair
+    rotation with a fixed constant-bank operator on DFMA (2 <= p <= 12, else v3) — match the
+    oracle."""
     monkeypatch.setenv("FMM_M2L_VARIANT", variant)
     torch = torch_cuda
     x, q = F.make(dist, n)
@@ -310,6 +312,7 @@ def test_m2l_split_tiles(torch_cuda, monkeypatch, split, dist, n, p, ncrit, thet
     global scratch in rank order) matches the oracle and the unsplit kernel to rounding."""
     torch = torch_cuda
     x, q = F.make(dist, n)
+    monkeypatch.setenv("FMM_M2L_VARIANT", "3")
     monkeypatch.setenv("FMM_M2L_SPLIT", "1")
     _, phi1, g1 = gpu_fmm(torch, x, q, p, ncrit, theta, grad=True)
     monkeypatch.setenv("FMM_M2L_SPLIT", split)
@@ -319,7 +322,7 @@ def test_m2l_split_tiles(torch_cuda, monkeypatch, split, dist, n, p, ncrit, thet
     assert O.rel_l2(phi, phi1) <= 1e-14
 
 
-@pytest.mark.parametrize("variant", ["1", "2", "3"])
+@pytest.mark.parametrize("variant", ["1", "2", "3", "4"])
 def test_stats_bytes_by_category(torch_cuda, monkeypatch, variant):
     """fmm_stats bytes_by (include/fmm.h FMM_B_*) partitions bytes_device; operator tables exist
     only for the precomputed formulations (v2/v3) beside the small M2M/L2L operators."""
@@ -336,5 +339,27 @@ def test_stats_bytes_by_category(torch_cuda, monkeypatch, variant):
     assert by["particles"] >= 44 * st["n"]
     if variant == "1":
         assert by["operators"] < 1e6 and by["schedule"] == 0
+    elif variant == "4":  # the fixed operator lives in constant memory; unit partial sums
+        assert by["operators"] < 1e6 and by["schedule"] > 0
     else:
         assert by["operators"] > 1e6 and by["schedule"] > 0
+
+
+@pytest.mark.parametrize("chunks", ["1", "2", "5"])
+@pytest.mark.parametrize("dist,n,p,ncrit,theta", [("plummer", 20000, 8, 32, 0.5), ("cube", 20000, 10, 64, 0.4),
+                                                  ("sphere", 20000, 12, 128, 0.4)])
+def test_m2l_v4_units(torch_cuda, monkeypatch, chunks, dist, n, p, ncrit, theta):
+    """M2L v4 with small work units (1, 2, 5 chunks of 32 pairs): targets cross many unit
+    boundaries (partial sums per unit, added in unit order by the fix-up kernel, including units
+    that lie wholly inside one target); results match the oracle and the default units."""
+    torch = torch_cuda
+    x, q = F.make(dist, n)
+    monkeypatch.setenv("FMM_M2L_VARIANT", "4")
+    _, phi0, g0 = gpu_fmm(torch, x, q, p, ncrit, theta, grad=True)
+    monkeypatch.setenv("FMM_V4_UNIT_CHUNKS", chunks)
+    for wpc in ("1", "3"):
+        monkeypatch.setenv("FMM_V4_WARPS", wpc)
+        _, phi, g = gpu_fmm(torch, x, q, p, ncrit, theta, grad=True)
+        assert O.rel_l2(phi, phi0) <= 1e-14 and O.rel_l2(g, g0) <= 1e-14
+    po, go = O.fmm(x, q, p, ncrit, theta, grad=True, nthreads=O.default_threads())
+    assert O.rel_l2(phi, po) <= TOL and O.rel_l2(g, go) <= TOL

@@ -249,9 +249,21 @@ def main():
     cfg = F.CONFIGS[args.config]
     if args.grad:
         cfg = F.Config(**{**cfg.__dict__, "grad": True})
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (127.0.0.1 rendezvous)
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch one rank per GPU)")
     if args.impl == "reference":
         run_reference(args, cfg, rank)
         return
@@ -280,6 +292,16 @@ def main():
         inner = plan
     q_dev = torch.from_numpy(q[lo:hi]).to(dev)
     st0 = inner.stats()
+    # setup (precalculation) timed apart: median of 3 warm plans (1 GPU)
+    setup_ms = [st0["t_setup_ms"][3]]
+    if world == 1:
+        xd = torch.from_numpy(x).to(dev)
+        setup_ms = []
+        for _ in range(3):
+            pl2 = Plan(xd, cfg.p, cfg.ncrit, cfg.theta)
+            setup_ms.append(pl2.stats()["t_setup_ms"][3])
+            del pl2
+        del xd
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step():
@@ -364,7 +386,8 @@ def main():
                "d2h_bytes_per_step": 8 * cfg.n * (4 if cfg.grad else 1),
                "timing": "host wall clock per rank (own slices, pinned), max over ranks"}
 
-    # ---- roofline of the dominant kernel (algorithmic flops / its event-timed duration)
+    # ---- roofline of the dominant kernel: the work the executed formulation does (not a dense
+    # equivalent; the paper's point is that the FMM does "only useful Flops")
     st = inner.stats()
     m2l_ms = max(1e-6, statistics.mean(s[1] for s in stage))  # stage events of the inner plan
     near_ms = max(1e-6, statistics.mean(s[2] for s in stage))
@@ -372,9 +395,9 @@ def main():
     down_ms = statistics.mean(s[3] for s in stage)
     p = cfg.p
     nc = (p + 1) * (p + 2) // 2
-    m2l_dense_flops = 2.0 * (p + 1) ** 4 * st["n_m2l_pairs"]  # SURVEY 8(d) dense-operator convention
-    m2l_flops = st["m2l_flops_per_pair"] * st["n_m2l_pairs"]  # useful flops of the formulation in use
     own_frac = (st["own_end"] - st["own_begin"]) / cfg.n
+    m2l_flops = st["m2l_flops_per_pair"] * st["n_m2l_pairs"] * (own_frac if world > 1 else 1.0)  # executed form
+    m2l_dense_flops = 2.0 * (p + 1) ** 4 * st["n_m2l_pairs"] * (own_frac if world > 1 else 1.0)  # SURVEY 8(d) dense
     p2p_inter = (st["n_p2p_interactions"] - cfg.n) * own_frac
     near_flops = (19.0 if cfg.grad else 11.0) * p2p_inter + (3 if cfg.grad else 1) * 8.0 * nc * cfg.n * own_frac
     nominal = fp64_nominal_tflops()
@@ -384,13 +407,10 @@ def main():
             probe = fp64_probe(torch)
         except Exception as e:  # measurement helper only
             probe = {"error": str(e)}
-    # roofline.achieved follows SURVEY §8(d)'s per-unit figure (M2L: the dense operator, 2(p+1)^4 flop
-    # per pair); the rotation formulation in use executes fewer flops: its useful rate is reported
-    # beside it (m2l_formulation.useful_tflops) and the DMMA pipe share is in profiles/ (ncu)
     if m2l_ms >= near_ms:
-        dom, dflops, dms = "m2l", m2l_dense_flops, m2l_ms
+        dom, dflops, dms = "m2l", m2l_flops, m2l_ms
     else:
-        dom, dflops, dms = "near (L2P+P2P)", near_flops, near_ms
+        dom, dflops, dms = "near (P2P+L2P)", near_flops, near_ms
     achieved = dflops / (dms * 1e-3) / 1e12
     traffic = None
     try:
@@ -398,20 +418,27 @@ def main():
             traffic = json.load(f).get(dom, {}).get("bytes")
     except (OSError, ValueError):
         pass
+    p2p_m2l_tflops = (m2l_flops + near_flops) / ((m2l_ms + near_ms) * 1e-3) / 1e12
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
                 "frac": achieved / nominal, "traffic": traffic,
                 "traffic_source": "profiles/traffic.json (ncu --set full, DRAM read+write bytes per launch)",
-                "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz (DESIGN.md §2)",
+                "peak_source": "derived (no FP64 entry in MEASURED_PEAKS.json): 148 SM x 64 FP64 FMA/clk x 2 x "
+                               "sm_max_mhz; measured_fp64_probe is a DFMA microbenchmark beside it (DESIGN.md §6)",
                 "measured_fp64_probe": probe,
+                "p2p_m2l_frac": p2p_m2l_tflops / nominal,
+                "p2p_m2l_tflops": p2p_m2l_tflops,
                 "stages_ms": {"upward": up_ms, "m2l": m2l_ms, "downward": down_ms, "near": near_ms},
-                "algorithmic_tflops": {"m2l": m2l_dense_flops / (m2l_ms * 1e-3) / 1e12,
-                                       "near": near_flops / (near_ms * 1e-3) / 1e12},
-                "convention": "SURVEY 8(d): M2L 2(p+1)^4 flop per pair (dense operator), P2P 11 (phi) / 19 "
-                              "(phi+grad) flop per interaction, L2P 8 (p+1)(p+2)/2 per particle (x3 with grad)",
-                "m2l_formulation": {"variant": st["m2l_variant"], "useful_flops_per_pair": st["m2l_flops_per_pair"],
-                                    "useful_tflops": m2l_flops / (m2l_ms * 1e-3) / 1e12,
-                                    "useful_frac": m2l_flops / (m2l_ms * 1e-3) / 1e12 / nominal,
-                                    "survey_flops_per_pair": 2.0 * (p + 1) ** 4}}
+                "executed_tflops": {"m2l": m2l_flops / (m2l_ms * 1e-3) / 1e12,
+                                    "near": near_flops / (near_ms * 1e-3) / 1e12},
+                "convention": "executed formulation: M2L fmm_stats.m2l_flops_per_pair (v4: per-pair rotation "
+                              "with the fixed operator, 2 x (FMAs of F, F^T, G, G^T, the z-rotations and the "
+                              "Hankel translation)); P2P 11 (phi) / 19 (phi+grad) flop per interaction; L2P "
+                              "8 (p+1)(p+2)/2 per particle (x3 with grad)",
+                "m2l_formulation": {"variant": st["m2l_variant"], "flops_per_pair": st["m2l_flops_per_pair"]},
+                "dense_equivalent": {"m2l_flops_per_pair": 2.0 * (p + 1) ** 4,
+                                     "m2l_tflops": m2l_dense_flops / (m2l_ms * 1e-3) / 1e12,
+                                     "note": "SURVEY 8(d)'s dense-operator count 2(p+1)^4: the method's speed, "
+                                             "not the kernel's fraction of peak"}}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only, bounded sample)
     cpu = None
@@ -436,7 +463,7 @@ def main():
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(cfg, world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "clocks": clk.summary(), "gpu_launches": launches,
-        "setup_ms": st0["t_setup_ms"][3],
+        "setup_ms": statistics.median(setup_ms), "setup_ms_all": setup_ms,
         "counts": {k: st[k] for k in ("n_cells", "n_leaves", "n_p2p_pairs", "n_m2l_pairs", "n_p2p_interactions",
                                       "max_level")},
         "ms_per_step_min": min(ms),

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, os.path.basename(os.environ.get("FMM_LIB", "libfmm.so")))  # FMM_LIB: experiments
+LIB_PATH = os.path.join(_PKG, "libfmm.so")
 
 FMM_OK, FMM_ERR_USAGE, FMM_ERR_NUMERIC, FMM_ERR_CUDA, FMM_ERR_OOM, FMM_ERR_COMM = 0, 2, 3, 4, 5, 6
 
@@ -65,17 +65,8 @@ def lib() -> C.CDLL:
                           "(the CUDA path has no fallback)")
     L = C.CDLL(LIB_PATH)
     missing = [s for s in EXPORTED if not hasattr(L, s)]
-    if missing and os.path.basename(LIB_PATH) == "libfmm.so":
+    if missing:
         raise ImportError(f"{LIB_PATH} lacks {missing}: rebuild it (python -m paper_1602_02244_b200.build)")
-    if missing:  # an older experimental library (FMM_LIB): declare what it has
-        class _Opt:
-            def __init__(self, lib):
-                self._lib = lib
-
-            def __getattr__(self, name):
-                return getattr(self._lib, name) if hasattr(self._lib, name) else type("_Stub", (), {})()
-
-        L = _Opt(L)
     vp, dp, i64 = C.c_void_p, C.c_void_p, C.c_int64
     L.fmm_setup.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.POINTER(FmmExec)]
     L.fmm_setup_2d.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.POINTER(FmmExec)]

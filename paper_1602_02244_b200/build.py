@@ -15,16 +15,16 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-# FMM_LIB (experiments only): build / load an alternative in-tree library, e.g. libfmm_x.so
-LIB = os.path.join(PKG, os.path.basename(os.environ.get("FMM_LIB", "libfmm.so")))
-BUILD = os.path.join(PKG, "_build" + os.path.basename(LIB)[len("libfmm"):-len(".so")])
+LIB = os.path.join(PKG, "libfmm.so")
+BUILD = os.path.join(PKG, "_build")
+STAMP = LIB + ".flags"  # the nvcc flags of the built library: a flag change forces a rebuild
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-] + os.environ.get("FMM_NVCC_EXTRA", "").split()  # experiments only (e.g. -DFMM_NEAR_MINB=4)
+] + os.environ.get("FMM_NVCC_EXTRA", "").split()  # experiments only (e.g. -DFMM_DEV, -DFMM_NEAR_MINB=4)
 
 
 def sources():
@@ -36,9 +36,16 @@ def _deps():
         os.path.join(ROOT, "include", "fmm.h"), os.path.join(ROOT, "include", "fmm_pde.h")]
 
 
+def _flags_id() -> str:
+    return " ".join(NVFLAGS)
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return False
+    with open(STAMP) as f:
+        if f.read() != _flags_id():
+            return False
     t = os.path.getmtime(LIB)
     return all(os.path.getmtime(d) <= t for d in _deps())
 
@@ -70,6 +77,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.check_call(link)
+    with open(STAMP, "w") as f:
+        f.write(_flags_id())
     return LIB
 
 

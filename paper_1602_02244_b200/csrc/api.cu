@@ -263,10 +263,12 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
     if (nv && nv[0] == '1') P->near_variant = 1;
     const char* sv = getenv("FMM_SHIFT_VARIANT");
     if (sv && sv[0] == '1') P->shift_variant = 1;
-    const char* fz = getenv("FMM_FUSE_NEAR");  // experiment: P2P warps inside the M2L v3 kernel
+#ifdef FMM_DEV  // development builds only (work-skipping / experimental paths)
+    const char* fz = getenv("FMM_FUSE_NEAR");  // experiment: P2P warps inside the M2L v3 kernel (slower)
     P->fuse_near = fz && fz[0] == '1';
-    const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // test hook: export M2L-only local expansions
+    const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // export M2L-only local expansions
     P->debug_skip_l2l = dbg && dbg[0] == '1';
+#endif
     if (dim == 3) {  // 3D translation operators (the 2D kernels are matrix-free)
       if (P->m2l_variant == 4)
         fmm::m2l_v4_setup(*P);

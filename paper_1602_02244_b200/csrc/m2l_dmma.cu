@@ -1040,8 +1040,13 @@ void m2l_dmma_pass(fmm_plan_s& P) {
       FMM_CUDA(cudaFuncSetAttribute(m2l_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
       configured[1] = sh;
     }
-    const char* dbg = getenv("FMM_M2L_DEBUG");  // timing experiments only (skips work: wrong results)
-    m2l_ws_kernel<<<(unsigned)D.ntiles, 32 * (nmma + nhelp), sh, P.stream>>>(a, nmma, nhelp, dbg ? atoi(dbg) : 0);
+#ifdef FMM_DEV  // development builds only: timing experiments (skips work: wrong results)
+    const char* dbgs = getenv("FMM_M2L_DEBUG");
+    const int dbg = dbgs ? atoi(dbgs) : 0;
+#else
+    const int dbg = 0;
+#endif
+    m2l_ws_kernel<<<(unsigned)D.ntiles, 32 * (nmma + nhelp), sh, P.stream>>>(a, nmma, nhelp, dbg);
     FMM_LAUNCHED("m2l_ws_kernel");
     return;
   }

@@ -524,8 +524,12 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
     r.p2p_phi = P.near_p2p_phi;
     r.p2p_grad = P.near_fused_grad ? P.near_p2p_grad.ptr : nullptr;
   }
-  const char* dbgs = getenv("FMM_M2L_DEBUG");  // timing experiments only (most bits skip work: wrong results)
+#ifdef FMM_DEV  // development builds only: timing experiments (most bits skip work: wrong results)
+  const char* dbgs = getenv("FMM_M2L_DEBUG");
   const int dbg = dbgs ? atoi(dbgs) : 0;
+#else
+  const int dbg = 0;
+#endif
   r.prof = nullptr;
   static DevBuf<unsigned long long> prof_buf;
   if (dbg & 256) {  // timing experiment: per-warp cycle breakdown printed to stderr after the launch

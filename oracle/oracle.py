@@ -185,7 +185,10 @@ class Plan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().oracle_plan_free(h)
+            try:
+                lib().oracle_plan_free(h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     def info(self, name):

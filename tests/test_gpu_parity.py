@@ -121,12 +121,38 @@ def test_expansions_and_outputs_match_oracle(torch_cuda, dist, n, p, ncrit, thet
     nm = np.linalg.norm(M, axis=1)
     nl = np.linalg.norm(L, axis=1)
     assert (np.linalg.norm(Mg - M, axis=1) <= 1e-13 * nm + 1e-300).all()
-    # 1e-11 per cell: Plummer-core leaves sum 100-175 M2L terms with cancellation; the
-    # GPU's scaled DMMA operators and the oracle's complex O(p^4) sums round differently
-    # (measured worst 1.7e-12; cells with one level difference agree to 4e-15). DESIGN.md R13.
-    assert (np.linalg.norm(Lg - L, axis=1) <= 1e-11 * nl + 1e-300).all()
+    # locals: SURVEY §8(c)'s 1e-12 per cell, or — for a cell whose sum cancels (Plummer-core
+    # leaves add 100-175 M2L terms) — a condition-aware bound (R13)
+    el = np.linalg.norm(Lg - L, axis=1)
+    flagged = np.nonzero(el > 1e-12 * nl + 1e-300)[0]
+    assert len(flagged) <= max(2, len(nl) // 500)
+    if len(flagged):
+        check_local_condition_bound(orc, p, M, L, Lg, flagged)
     assert O.rel_l2(phi, po) <= TOL
     assert O.rel_l2(g, go) <= TOL
+
+
+def check_local_condition_bound(orc, p, M, L, Lg, cells):
+    """Condition-aware gate for local expansions (R13). For target cell A, the GPU's
+    own rounding error — its difference from the oracle minus the L2L shift of its parent's
+    difference (gated at the parent) — must satisfy
+        ||dL_A - L2L(dL_parent)|| <= c u (sum_B ||T_AB M_B|| + ||L2L(L_parent)||),
+    u = 2^-53, c = 100 (p+1)^2 (the operation depth of one rotation-form pair, generously): the
+    terms' magnitudes, not the cancelled sum's, set the attainable accuracy. The terms are the
+    oracle's own operators (m2l, l2l) on the oracle's expansions."""
+    cc = orc.cells()
+    center, parent = cc["center"], cc["parent"]
+    _, m2l = orc.lists()
+    u = 2.0**-53
+    for a in cells:
+        srcs = m2l[m2l[:, 0] == a, 1]
+        s = sum(np.linalg.norm(O.m2l(M[b], center[b], center[a], p)) for b in srcs)
+        d = Lg[a] - L[a]
+        par = parent[a]
+        if par >= 0:
+            s += np.linalg.norm(O.l2l(L[par], center[par], center[a], p))
+            d = d - O.l2l(Lg[par] - L[par], center[par], center[a], p)
+        assert np.linalg.norm(d) <= 100 * (p + 1) ** 2 * u * s, (a, np.linalg.norm(d), s)
 
 
 def test_c1_against_direct_and_survey_truncation(torch_cuda):
@@ -217,15 +243,16 @@ def test_usage_and_numeric_errors(torch_cuda):
     assert np.isfinite(phi.numpy()).all()
 
 
-FULL = [("c2", 2000), ("c3", 2000), ("c4", 1000), ("l3", 2000)]
+# 10^4 sampled targets (seed 12345) at every BASELINE config, configs[4] included
+FULL = [("c2", 10_000), ("c3", 10_000), ("c4", 10_000), ("c5", 10_000), ("l3", 10_000)]
 
 
 @pytest.mark.parametrize("name,k", FULL)
 def test_full_size_sampled_parity(torch_cuda, name, k):
     """BASELINE.json full sizes, bench launch configuration, on a seeded target sample
     computed one by one by the oracle's sampled-target mode (A15)."""
-    if name == "c4" and os.environ.get("FMM_SKIP_C4"):
-        pytest.skip("FMM_SKIP_C4 set")
+    if name in ("c4", "c5") and os.environ.get("FMM_SKIP_LARGE"):
+        pytest.skip("FMM_SKIP_LARGE set")
     torch = torch_cuda
     cfg = F.CONFIGS[name]
     x, q = F.make_config(name)
@@ -290,7 +317,8 @@ def test_near_variants(torch_cuda, monkeypatch, variant, dist, n, p, ncrit, thet
 def test_shift_variants(torch_cuda, monkeypatch, variant, par, dist, n, p, ncrit, theta):
     """M2M / L2L (north_star (3)): v1 block per parent with the branchy term sums and v2 the
     level-independent scaled operators A(+,+,+) on DMMA with octant sign maps
-    give the oracle's multipoles per cell to 1e-13 and its local expansions to 1e-11."""
+    give the oracle's multipoles per cell to 1e-13 and its local expansions to 1e-12 (or the
+    condition-aware bound of check_local_condition_bound)."""
     monkeypatch.setenv("FMM_SHIFT_VARIANT", variant)
     monkeypatch.setenv("FMM_SHIFT_PAR", par)
     torch = torch_cuda
@@ -301,7 +329,11 @@ def test_shift_variants(torch_cuda, monkeypatch, variant, par, dist, n, p, ncrit
     M, L = orc.expansions()
     Mg, Lg = pl.export("M"), pl.export("L")
     assert (np.linalg.norm(Mg - M, axis=1) <= 1e-13 * np.linalg.norm(M, axis=1) + 1e-300).all()
-    assert (np.linalg.norm(Lg - L, axis=1) <= 1e-11 * np.linalg.norm(L, axis=1) + 1e-300).all()
+    nl = np.linalg.norm(L, axis=1)
+    flagged = np.nonzero(np.linalg.norm(Lg - L, axis=1) > 1e-12 * nl + 1e-300)[0]
+    assert len(flagged) <= max(2, len(nl) // 500)
+    if len(flagged):
+        check_local_condition_bound(orc, p, M, L, Lg, flagged)
     assert O.rel_l2(phi, po) <= TOL and O.rel_l2(g, go) <= TOL
 
 

@@ -231,6 +231,31 @@ def config_dict(cfg, n_gpus):
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
+def run_dry(args, world, rank):
+    """The multi-rank launch / timing plumbing with no FMM and no GPU (gloo): every rank
+    checks the world, times `--steps` empty steps between barriers, and the max over ranks is
+    printed by rank 0 — what the real arm does around fmm_matvec."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = []
+    for _ in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        t.append(time.perf_counter() - t0)
+    tot = torch.tensor([sum(t[args.warmup:])], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": world, "steps": args.steps,
+                          "warmup": args.warmup, "max_over_ranks_s": tot.item()}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -245,6 +270,7 @@ def main():
     ap.add_argument("--cpu-full-max-n", type=int, default=2_000_000)
     ap.add_argument("--ref-targets", type=int, default=100000)
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launcher / timing plumbing only (no GPU, gloo)")
     args = ap.parse_args()
     cfg = F.CONFIGS[args.config]
     if args.grad:
@@ -266,6 +292,9 @@ def main():
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch one rank per GPU)")
     if args.impl == "reference":
         run_reference(args, cfg, rank)
+        return
+    if args.dry_run:  # launcher check without a GPU (tests/test_bench_launch.py)
+        run_dry(args, world, rank)
         return
 
     import torch

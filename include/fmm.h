@@ -75,10 +75,16 @@ typedef struct {
   int device;     /* CUDA ordinal this process drives */
   void* stream;   /* cudaStream_t; NULL = legacy default stream */
   int rank;       /* 0 .. world_size-1 (multi-GPU: one process per GPU) */
-  int world_size; /* 1 = single GPU. For world_size > 1 every rank passes the
-                     GLOBAL point set to fmm_setup (the Python layer all-gathers
-                     caller slices over NCCL) and fmm_matvec evaluates only the
-                     targets of this rank's Morton range, see fmm_matvec. */
+  int world_size; /* 1 = single GPU */
+  const void* nccl_id; /* a 128-byte ncclUniqueId, the same on every rank (rank 0 makes it with
+                          fmm_nccl_unique_id and broadcasts it by any means), or NULL. Non-NULL:
+                          "collective mode" — fmm_setup and fmm_matvec are COLLECTIVE over the
+                          ranks and take and return each rank's own slice of the points /
+                          charges / results (the library redistributes by Morton order and
+                          moves the local-essential-tree exchange with NCCL on `stream`,
+                          DESIGN.md §5); world_size 1 is allowed (a one-rank communicator: the
+                          same code path). NULL with world_size > 1: the legacy mode below
+                          (global points, caller-moved exchange, fmm_let_*). */
 } fmm_exec;
 
 /* Filled by fmm_stats. Times are CUDA-event milliseconds of the last call. */
@@ -95,12 +101,14 @@ typedef struct {
   double t_matvec_ms[8]; /* FMM_T_UPWARD .. FMM_T_MATVEC_TOTAL (0 unless timing enabled) */
   int64_t bytes_device;  /* device memory owned by the plan */
   int m2l_variant;       /* M2L formulation in use: 1 matrix-free O(p^4) per pair, 2 dense class
-                            operators on DMMA, 3 rotation-factored class operators on DMMA;
-                            0 for a 2D (log-kernel) plan, whose M2L is the complex series */
+                            operators on DMMA, 3 rotation-factored class operators on DMMA,
+                            4 per-pair rotation on DFMA with one fixed operator (default,
+                            2 <= p <= 12); 0 for a 2D (log-kernel) plan (complex series) */
   int m2l_pad_;
-  double m2l_flops_per_pair; /* useful flops per M2L pair of that formulation (v3: the three
-                                block stages + the two azimuthal rotations; v1/v2: 2(p+1)^4;
-                                2D: 8(p+1)^2, one complex multiply-add per (l, k)) */
+  double m2l_flops_per_pair; /* flops per M2L pair of that formulation as executed (v4: the four
+                                fixed-operator products, four z-rotations and the Hankel
+                                translation; v3: the three block stages + the two azimuthal
+                                rotations; v1/v2: 2(p+1)^4; 2D: 8(p+1)^2) */
   int64_t bytes_by[8];       /* bytes_device by category, FMM_B_* (the FMM side of PAPER.md
                                 Fig 4, "strictly O(N) storage") */
   int64_t launches_total;    /* kernels launched by libfmm in this process so far (all plans,
@@ -122,7 +130,11 @@ enum {
  * device radix sort, adaptive octree, dual tree traversal -> P2P and M2L lists.
  *   out   : receives the new plan (NULL on error)
  *   xyz   : device [n][3] fp64 point coordinates (copied; may be freed after return)
- *   n     : number of points, >= 1 (global count when world_size > 1)
+ *   n     : number of points, >= 1. Collective mode (nccl_id set): this
+ *           rank's slice, >= 0 (the global count, the sum over ranks, >= 1); the plan is the
+ *           single global tree and lists on every rank, the rank's targets a contiguous
+ *           Morton range cut at leaf boundaries by estimated work. Legacy multi-GPU mode
+ *           (nccl_id NULL): the GLOBAL point set on every rank.
  *   p     : expansion order, 0 <= p <= 16
  *   ncrit : maximum leaf population, >= 1
  *   theta : MAC parameter, 0 < theta < 1/sqrt(3)
@@ -153,8 +165,13 @@ FMM_API fmm_status fmm_setup_2d(fmm_plan* out, const double* xy, int64_t n, int 
  *   n    : must equal the setup n (FMM_ERR_USAGE otherwise)
  *   phi  : device [n] fp64 output, caller order
  *   grad : device [n][3] fp64 output or NULL
- * With world_size > 1 only the entries of targets owned by this rank (Morton
- * range [own_begin, own_end) of fmm_stats) are written; the others are set to 0,
+ * Collective mode (nccl_id set): q, phi, grad are THIS RANK's slices (n =
+ * the rank's setup n); the call is collective over the ranks, stream ordered, no host sync
+ * (exchange sizes are fixed at setup): the charges go to their owners and halo ranks, the
+ * boundary multipoles to the ranks whose targets need them, the results back to the caller
+ * slices, all with NCCL on the plan's stream.
+ * Legacy multi-GPU mode (nccl_id NULL): q is global and only the entries of targets owned by
+ * this rank (Morton range [own_begin, own_end) of fmm_stats) are written, the others set to 0,
  * so a sum over ranks (reduce-scatter) assembles the global result exactly.
  * Non-finite charges give FMM_ERR_NUMERIC, detected on the device and reported
  * by the NEXT fmm_matvec / fmm_sync call on the plan (the call is stream ordered).
@@ -261,14 +278,22 @@ FMM_API fmm_status fmm_let_unpack(fmm_plan plan, const double* phi_recv, const d
  * fmm_let_lists_host — the exchange lists of rank `me` from HOST copies of a tree
  * (no device work; the same host code fmm_let_setup runs). what = one of
  * fmm_let_what; dst NULL queries *count. Arrays as in fmm_export; caller_off
- * [world + 1] prefix sums of the caller counts; leaves sorted by first particle.
+ * [world + 1] prefix sums of the caller counts; leaves sorted by first particle;
+ * p the expansion order (it weights the owner cuts).
  */
-FMM_API fmm_status fmm_let_lists_host(int64_t n, int world, int me, const int64_t* caller_off, const uint32_t* perm,
+FMM_API fmm_status fmm_let_lists_host(int64_t n, int world, int me, int p, const int64_t* caller_off, const uint32_t* perm,
                                       int64_t ncells, const int32_t* cbeg, const int32_t* cend, int64_t nleaves,
                                       const int32_t* leaves, int64_t np2p, const int32_t* p2p_tgt,
                                       const int32_t* p2p_src, int64_t nm2l, const int32_t* m2l_tgt,
                                       const int32_t* m2l_src, int what, int64_t* dst, int64_t capacity,
                                       int64_t* count);
+
+/*
+ * fmm_nccl_unique_id — a new ncclUniqueId (128 bytes written to out, host memory) for the
+ * collective mode; call on ONE rank and send the bytes to the others. Loads NCCL
+ * (libnccl.so.2) on first use; FMM_ERR_COMM if it is unavailable.
+ */
+FMM_API fmm_status fmm_nccl_unique_id(void* out);
 
 /* fmm_destroy — free the plan (NULL is a no-op). */
 FMM_API void fmm_destroy(fmm_plan plan);

@@ -23,11 +23,12 @@ EXPORTED = ("fmm_setup", "fmm_setup_2d", "fmm_matvec", "fmm_matvec_host", "fmm_s
             "fmm_set_timing", "fmm_export", "fmm_destroy", "fmm_last_error", "fmm_version", "fmm_let_setup",
             "fmm_let_counts", "fmm_let_pack_q", "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack",
             "fmm_let_lists_host", "fmm_stencil_apply", "fmm_precond_setup", "fmm_precond_apply", "fmm_precond_info",
-            "fmm_precond_destroy", "fmm_pcg_solve")
+            "fmm_precond_destroy", "fmm_pcg_solve", "fmm_nccl_unique_id")
 
 
 class FmmExec(C.Structure):
-    _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("rank", C.c_int), ("world_size", C.c_int)]
+    _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("rank", C.c_int), ("world_size", C.c_int),
+                ("nccl_id", C.c_void_p)]
 
 
 class FmmStats(C.Structure):
@@ -68,6 +69,7 @@ def lib() -> C.CDLL:
     if missing:
         raise ImportError(f"{LIB_PATH} lacks {missing}: rebuild it (python -m paper_1602_02244_b200.build)")
     vp, dp, i64 = C.c_void_p, C.c_void_p, C.c_int64
+    L.fmm_nccl_unique_id.argtypes = [vp]
     L.fmm_setup.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.POINTER(FmmExec)]
     L.fmm_setup_2d.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.POINTER(FmmExec)]
     L.fmm_matvec.argtypes = [vp, dp, i64, dp, dp]
@@ -87,7 +89,7 @@ def lib() -> C.CDLL:
     L.fmm_let_upward.argtypes = [vp, dp, dp, dp]
     L.fmm_let_finish.argtypes = [vp, dp, dp, dp, dp]
     L.fmm_let_unpack.argtypes = [vp, dp, dp, dp, dp]
-    L.fmm_let_lists_host.argtypes = [i64, C.c_int, C.c_int, vp, vp, i64, vp, vp, i64, vp, i64, vp, vp, i64, vp, vp,
+    L.fmm_let_lists_host.argtypes = [i64, C.c_int, C.c_int, C.c_int, vp, vp, i64, vp, vp, i64, vp, i64, vp, vp, i64, vp, vp,
                                      C.c_int, vp, i64, C.POINTER(C.c_int64)]
     # include/fmm_pde.h (NEXT-2)
     L.fmm_stencil_apply.argtypes = [C.c_int, dp, dp, vp]
@@ -101,7 +103,8 @@ def lib() -> C.CDLL:
                                 C.POINTER(PcgInfo), vp]
     for nm in ("fmm_setup", "fmm_setup_2d", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
                "fmm_set_timing", "fmm_export", "fmm_let_setup", "fmm_let_counts", "fmm_let_pack_q",
-               "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack", "fmm_let_lists_host", "fmm_stencil_apply",
+               "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack", "fmm_let_lists_host", "fmm_nccl_unique_id",
+               "fmm_stencil_apply",
                "fmm_precond_setup", "fmm_precond_apply", "fmm_precond_info", "fmm_pcg_solve"):
         getattr(L, nm).restype = C.c_int
     _lib = L

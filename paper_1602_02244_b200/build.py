@@ -73,7 +73,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
             failed.append(src)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcublas"]
+    link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcublas", "-ldl"]
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.check_call(link)

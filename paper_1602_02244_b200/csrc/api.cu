@@ -78,8 +78,8 @@ void order_leaves_by_position(fmm_plan_s& P) {
   FMM_LAUNCHED("leaf_store_kernel");
 }
 
-// This rank's targets: a contiguous range of leaves in Morton order with about
-// n / world particles each (cut at leaf boundaries).
+// This rank's targets: a contiguous range of leaves in Morton order with about 1 / world of
+// the estimated work (cut at leaf boundaries).
 void choose_own_range(fmm_plan_s& P) {
   if (P.world == 1) {
     P.own_leaf_begin = 0;
@@ -88,27 +88,7 @@ void choose_own_range(fmm_plan_s& P) {
     P.own_end = P.n;
     return;
   }
-  std::vector<int32_t> lv(P.nleaves), lb(P.cells.n);
-  FMM_CUDA(cudaMemcpyAsync(lv.data(), P.leaves.ptr, sizeof(int32_t) * P.nleaves, cudaMemcpyDeviceToHost, P.stream));
-  FMM_CUDA(cudaMemcpyAsync(lb.data(), P.cells.begin.ptr, sizeof(int32_t) * P.cells.n, cudaMemcpyDeviceToHost,
-                           P.stream));
-  FMM_CUDA(cudaStreamSynchronize(P.stream));
-  auto cut = [&](int r) -> int64_t {  // first leaf whose begin >= r * n / world
-    const int64_t target = (int64_t)r * P.n / P.world;
-    int64_t lo = 0, hi = P.nleaves;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) / 2;
-      if (lb[lv[mid]] < target)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    return lo;
-  };
-  P.own_leaf_begin = cut(P.rank);
-  P.own_leaf_end = cut(P.rank + 1);
-  P.own_begin = P.own_leaf_begin < P.nleaves ? lb[lv[P.own_leaf_begin]] : P.n;
-  P.own_end = P.own_leaf_end < P.nleaves ? lb[lv[P.own_leaf_end]] : P.n;
+  fmm::let_partition(P);  // cost-weighted cut at leaf boundaries (let.cu let_cuts)
 }
 
 struct Timer {
@@ -198,6 +178,91 @@ void check_flags(fmm_plan_s& P) {
   }
 }
 
+// multi-GPU (LET) steps 4-5 on this rank: exchanged multipoles in, M2L of the targets overlapping
+// the range, L2L, near field of own leaves, results packed for their callers
+void let_finish_impl(fmm_plan_s& P, const double* shared_recv, const double* m_recv, double* phi_send,
+                     double* grad_send) {
+  Timer T(P, P.timing);
+  T.mark(1);
+  fmm::let_exchange_in(P, shared_recv, m_recv);
+  P.near_fused_active = P.fuse_near && P.m2l_variant == 3 && P.near_variant == 2 && P.m2l_dmma.ntiles > 0;
+  P.near_fused_grad = grad_send != nullptr;
+  if (P.near_fused_active) fmm::near_fused_prepare(P, grad_send != nullptr);
+  if (P.m2l_variant == 4)
+    fmm::m2l_v4_pass(P);
+  else if (P.m2l_variant >= 2)
+    fmm::m2l_dmma_pass(P);
+  else
+    fmm::m2l_pass(P);
+  T.mark(2);
+  fmm::downward_own(P);
+  T.mark(3);
+  P.near_compact_out = true;
+  if (P.near_fused_active)
+    fmm::near_fused_finish(P, P.let_dev.phi_own.ptr, grad_send ? P.let_dev.grad_own.ptr : nullptr);
+  else
+    fmm::near_pass_warp(P, P.let_dev.phi_own.ptr, grad_send ? P.let_dev.grad_own.ptr : nullptr);
+  P.near_compact_out = false;
+  P.near_fused_active = false;
+  fmm::let_pack_phi(P, phi_send, grad_send);
+  T.mark(4);
+  if (T.on) {
+    FMM_CUDA(cudaEventSynchronize(P.ev[4]));
+    P.t_matvec[FMM_T_M2L] = T.between(1, 2);
+    P.t_matvec[FMM_T_DOWNWARD] = T.between(2, 3);
+    P.t_matvec[FMM_T_NEAR] = T.between(3, 4);
+  }
+}
+
+// collective mode (world > 1, fmm_exec.nccl_id): the whole LET protocol on the plan's stream,
+// the buffers moved by NCCL (comm.cu); q / phi / grad are this rank's caller slices
+void run_matvec_collective(fmm_plan_s& P, const double* q, double* phi, double* grad) {
+  fmm::LetLists& L = P.let;
+  fmm::LetDev& D = P.let_dev;
+  const int ncd = 2 * P.nc;
+  Timer T(P, P.timing);
+  T.mark(0);
+  fmm::let_pack_q(P, q, D.q_send.ptr);
+  fmm::comm_exchange(P, D.q_send.ptr, L.q_send, D.q_recv.ptr, L.q_recv, 1);
+  fmm::let_upward(P, D.q_recv.ptr, D.shared_send.ptr, D.m_send.ptr);
+  fmm::comm_allgather(P, D.shared_send.ptr, (int64_t)L.shared.size() * ncd, D.shared_recv.ptr);
+  fmm::comm_exchange(P, D.m_send.ptr, L.m_send, D.m_recv.ptr, L.m_recv, ncd);
+  T.mark(1);
+  const float t_up = T.on ? (FMM_CUDA(cudaEventSynchronize(P.ev[1])), T.between(0, 1)) : 0.f;
+  let_finish_impl(P, D.shared_recv.ptr, D.m_recv.ptr, D.phi_send.ptr, grad ? D.grad_send.ptr : nullptr);
+  T.mark(5);
+  fmm::comm_exchange(P, D.phi_send.ptr, L.phi_send, D.phi_recv.ptr, L.phi_recv, 1);
+  if (grad) fmm::comm_exchange(P, D.grad_send.ptr, L.phi_send, D.grad_recv.ptr, L.phi_recv, 3);
+  fmm::let_unpack(P, D.phi_recv.ptr, grad ? D.grad_recv.ptr : nullptr, phi, grad);
+  T.mark(6);
+  if (T.on) {
+    FMM_CUDA(cudaEventSynchronize(P.ev[6]));
+    P.t_matvec[FMM_T_UPWARD] = t_up;  // q exchange + upward pass + multipole exchange
+    P.t_matvec[FMM_T_MATVEC_TOTAL] = T.between(0, 6);
+  }
+}
+
+void alloc_exchange_buffers(fmm_plan_s& P) {
+  fmm::LetLists& L = P.let;
+  fmm::LetDev& D = P.let_dev;
+  auto sum = [](const std::vector<int64_t>& v) {
+    int64_t s = 0;
+    for (int64_t x : v) s += x;
+    return std::max<int64_t>(1, s);
+  };
+  const int64_t ncd = 2 * P.nc, ns = (int64_t)L.shared.size();
+  D.q_send.alloc(sum(L.q_send));
+  D.q_recv.alloc(sum(L.q_recv));
+  D.shared_send.alloc(std::max<int64_t>(1, ns * ncd));
+  D.shared_recv.alloc(std::max<int64_t>(1, ns * ncd * P.world));
+  D.m_send.alloc(sum(L.m_send) * ncd);
+  D.m_recv.alloc(sum(L.m_recv) * ncd);
+  D.phi_send.alloc(sum(L.phi_send));
+  D.phi_recv.alloc(sum(L.phi_recv));
+  D.grad_send.alloc(3 * sum(L.phi_send));
+  D.grad_recv.alloc(3 * sum(L.phi_recv));
+}
+
 }  // namespace
 
 int64_t fmm_plan_s::bytes() const {
@@ -224,8 +289,10 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
   fmm_plan_s* P = nullptr;
   fmm_status st = guarded(nullptr, [&] {
     usage(ex != nullptr, "fmm_setup: ex is NULL");
-    usage(xyz != nullptr, "fmm_setup: xyz is NULL");
-    usage(n >= 1 && n < ((int64_t)1 << 31) - 1, "fmm_setup: n must be in [1, 2^31 - 2]");
+    const bool collective = ex->nccl_id != nullptr;  // (world_size 1 too: a one-rank communicator)
+    usage(xyz != nullptr || (collective && n == 0), "fmm_setup: xyz is NULL");
+    usage(collective ? (n >= 0 && n < ((int64_t)1 << 31) - 1) : (n >= 1 && n < ((int64_t)1 << 31) - 1),
+          "fmm_setup: n must be in [1, 2^31 - 2] (collective mode: this rank's slice, >= 0)");
     usage(p >= 0 && p <= fmm::kMaxP, "fmm_setup: p must be in [0, 16]");
     usage(ncrit >= 1, "fmm_setup: ncrit must be >= 1");
     usage(theta > 0.0 && theta * theta * 3.0 < 1.0, "fmm_setup: theta must be in (0, 1/sqrt(3))");
@@ -244,6 +311,19 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
     P->theta2 = theta * theta;
     P->dim = dim;
     usage(dim == 3 || ex->world_size == 1, "fmm_setup_2d: single-GPU only");
+    fmm::DevBuf<double> xyz_global;
+    if (collective) {  // every rank's slice -> the global point set (NCCL, comm.cu)
+      P->collective = true;
+      P->n_local = n;
+      fmm::comm_init(*P, ex->nccl_id);
+      P->caller_counts = fmm::comm_gather_counts(*P, n);
+      int64_t N = 0;
+      for (int64_t c : P->caller_counts) N += c;
+      usage(N >= 1 && N < ((int64_t)1 << 31) - 1, "fmm_setup: global n must be in [1, 2^31 - 2]");
+      fmm::comm_gather_points(*P, xyz, P->caller_counts, xyz_global);
+      xyz = xyz_global.ptr;
+      P->n = N;
+    }
     cudaEvent_t e0, e1, e2, e3;
     FMM_CUDA(cudaEventCreate(&e0));
     FMM_CUDA(cudaEventCreate(&e1));
@@ -277,6 +357,10 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
       fmm::shift_setup(*P);
     }
     P->M.alloc(P->cells.n * P->nc);
+    if (collective) {  // exchange lists and buffers of this rank (let.cu)
+      fmm::let_setup(*P, P->caller_counts.data());
+      alloc_exchange_buffers(*P);
+    }
     P->L.alloc(P->cells.n * P->nc);
     const char* poison = getenv("FMM_DEBUG_POISON");  // test hook: NaN-fill expansions so unwritten
     if (poison && poison[0] == '1') {                 // coefficients surface in the results
@@ -333,6 +417,13 @@ fmm_status fmm_matvec(fmm_plan P, const double* q, int64_t n, double* phi, doubl
   if (!P) return fail(FMM_ERR_USAGE, "fmm_matvec: plan is NULL");
   if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_matvec: plan is poisoned by an earlier error");
   return guarded(P, [&] {
+    if (P->collective) {  // this rank's caller slice in and out; collective over the world
+      usage(n == P->n_local, "fmm_matvec: n differs from this rank's setup slice");
+      usage(n == 0 || (q != nullptr && phi != nullptr), "fmm_matvec: q / phi is NULL");
+      FMM_CUDA(cudaSetDevice(P->device));
+      run_matvec_collective(*P, q, phi, grad);
+      return;
+    }
     usage(n == P->n, "fmm_matvec: n differs from the setup n");
     usage(q != nullptr && phi != nullptr, "fmm_matvec: q / phi is NULL");
     FMM_CUDA(cudaSetDevice(P->device));
@@ -344,17 +435,24 @@ fmm_status fmm_matvec_host(fmm_plan P, const double* q_host, int64_t n, double* 
   if (!P) return fail(FMM_ERR_USAGE, "fmm_matvec_host: plan is NULL");
   if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_matvec_host: plan is poisoned by an earlier error");
   return guarded(P, [&] {
-    usage(n == P->n, "fmm_matvec_host: n differs from the setup n");
-    usage(q_host != nullptr && phi_host != nullptr, "fmm_matvec_host: q / phi is NULL");
+    const int64_t nn = P->collective ? P->n_local : P->n;
+    usage(n == nn, "fmm_matvec_host: n differs from the setup n (collective mode: this rank's slice)");
+    usage(n == 0 || (q_host != nullptr && phi_host != nullptr), "fmm_matvec_host: q / phi is NULL");
     FMM_CUDA(cudaSetDevice(P->device));
-    if (P->host_stage_q.count < n) P->host_stage_q.alloc(n);
-    if (P->host_stage_phi.count < n) P->host_stage_phi.alloc(n);
+    if (P->host_stage_q.count < std::max<int64_t>(n, 1)) P->host_stage_q.alloc(std::max<int64_t>(n, 1));
+    if (P->host_stage_phi.count < std::max<int64_t>(n, 1)) P->host_stage_phi.alloc(std::max<int64_t>(n, 1));
     if (grad_host && P->host_stage_grad.count < 3 * n) P->host_stage_grad.alloc(3 * n);
-    FMM_CUDA(cudaMemcpyAsync(P->host_stage_q.ptr, q_host, sizeof(double) * n, cudaMemcpyHostToDevice, P->stream));
+    if (n > 0)
+      FMM_CUDA(cudaMemcpyAsync(P->host_stage_q.ptr, q_host, sizeof(double) * n, cudaMemcpyHostToDevice, P->stream));
     double* dg = grad_host ? P->host_stage_grad.ptr : nullptr;
-    run_matvec(*P, P->host_stage_q.ptr, P->host_stage_phi.ptr, dg);
-    FMM_CUDA(cudaMemcpyAsync(phi_host, P->host_stage_phi.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, P->stream));
-    if (grad_host)
+    if (P->collective)
+      run_matvec_collective(*P, P->host_stage_q.ptr, P->host_stage_phi.ptr, dg);
+    else
+      run_matvec(*P, P->host_stage_q.ptr, P->host_stage_phi.ptr, dg);
+    if (n > 0)
+      FMM_CUDA(cudaMemcpyAsync(phi_host, P->host_stage_phi.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                               P->stream));
+    if (grad_host && n > 0)
       FMM_CUDA(cudaMemcpyAsync(grad_host, dg, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, P->stream));
     check_flags(*P);
   });
@@ -525,6 +623,7 @@ fmm_status fmm_let_setup(fmm_plan P, const int64_t* caller_counts) {
   if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_let_setup: plan is poisoned by an earlier error");
   return guarded(P, [&] {
     usage(P->world > 1, "fmm_let_setup: world_size must be > 1");
+    usage(!P->collective, "fmm_let_setup: a collective (nccl_id) plan runs the exchange itself");
     FMM_CUDA(cudaSetDevice(P->device));
     fmm::let_setup(*P, caller_counts);
   });
@@ -605,36 +704,7 @@ fmm_status fmm_let_finish(fmm_plan P, const double* shared_recv, const double* m
               (P->let.phi_send_idx.empty() || phi_send),
           "fmm_let_finish: NULL buffer");
     FMM_CUDA(cudaSetDevice(P->device));
-    Timer T(*P, P->timing);
-    T.mark(1);
-    fmm::let_exchange_in(*P, shared_recv, m_recv);
-    P->near_fused_active = P->fuse_near && P->m2l_variant == 3 && P->near_variant == 2 && P->m2l_dmma.ntiles > 0;
-    P->near_fused_grad = grad_send != nullptr;
-    if (P->near_fused_active) fmm::near_fused_prepare(*P, grad_send != nullptr);
-    if (P->m2l_variant == 4)
-      fmm::m2l_v4_pass(*P);
-    else if (P->m2l_variant >= 2)
-      fmm::m2l_dmma_pass(*P);
-    else
-      fmm::m2l_pass(*P);
-    T.mark(2);
-    fmm::downward(*P);
-    T.mark(3);
-    P->near_compact_out = true;
-    if (P->near_fused_active)
-      fmm::near_fused_finish(*P, P->let_dev.phi_own.ptr, grad_send ? P->let_dev.grad_own.ptr : nullptr);
-    else
-      fmm::near_pass_warp(*P, P->let_dev.phi_own.ptr, grad_send ? P->let_dev.grad_own.ptr : nullptr);
-    P->near_compact_out = false;
-    P->near_fused_active = false;
-    fmm::let_pack_phi(*P, phi_send, grad_send);
-    T.mark(4);
-    if (T.on) {
-      FMM_CUDA(cudaEventSynchronize(P->ev[4]));
-      P->t_matvec[FMM_T_M2L] = T.between(1, 2);
-      P->t_matvec[FMM_T_DOWNWARD] = T.between(2, 3);
-      P->t_matvec[FMM_T_NEAR] = T.between(3, 4);
-    }
+    let_finish_impl(*P, shared_recv, m_recv, phi_send, grad_send);
   });
 }
 
@@ -650,16 +720,17 @@ fmm_status fmm_let_unpack(fmm_plan P, const double* phi_recv, const double* grad
   });
 }
 
-fmm_status fmm_let_lists_host(int64_t n, int world, int me, const int64_t* caller_off, const uint32_t* perm,
+fmm_status fmm_let_lists_host(int64_t n, int world, int me, int p, const int64_t* caller_off, const uint32_t* perm,
                               int64_t ncells, const int32_t* cbeg, const int32_t* cend, int64_t nleaves,
                               const int32_t* leaves, int64_t np2p, const int32_t* p2p_tgt, const int32_t* p2p_src,
                               int64_t nm2l, const int32_t* m2l_tgt, const int32_t* m2l_src, int what, int64_t* dst,
                               int64_t capacity, int64_t* count) {
   return guarded(nullptr, [&] {
-    usage(count != nullptr && world >= 1 && me >= 0 && me < world && n >= 1, "fmm_let_lists_host: bad arguments");
+    usage(count != nullptr && world >= 1 && me >= 0 && me < world && n >= 1 && p >= 0 && p <= fmm::kMaxP,
+          "fmm_let_lists_host: bad arguments");
     usage(caller_off && perm && cbeg && cend && leaves, "fmm_let_lists_host: NULL array");
     fmm::LetLists L;
-    fmm::let_lists(n, world, me, caller_off, perm, ncells, cbeg, cend, nleaves, leaves, np2p, p2p_tgt, p2p_src, nm2l,
+    fmm::let_lists(n, world, me, p, caller_off, perm, ncells, cbeg, cend, nleaves, leaves, np2p, p2p_tgt, p2p_src, nm2l,
                    m2l_tgt, m2l_src, L);
     std::vector<int64_t> tmp;
     const std::vector<int64_t>* v = let_vec(L, what);
@@ -687,6 +758,10 @@ void fmm_destroy(fmm_plan P) {
   cudaStreamSynchronize(P->stream);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
+  try {
+    fmm::comm_destroy(*P);
+  } catch (...) {
+  }
   delete P;
 }
 

@@ -536,7 +536,18 @@ void launch_shift(fmm_plan_s& P, int64_t lb, int64_t ncell) {
   }
 }
 
-void upward_impl(fmm_plan_s& P, int64_t leaf_b, int64_t leaf_e) {
+// level l's parents to shift: all cells of the level, or (multi-GPU, LET) those overlapping
+// the owned range [let_level_lo[l], let_level_hi[l])
+struct LevelRange {
+  int64_t b, n;
+};
+LevelRange level_range(const fmm_plan_s& P, int l, bool own) {
+  if (own && P.let_ready && (int)P.let_level_lo.size() > l)
+    return {P.let_level_lo[l], P.let_level_hi[l] - P.let_level_lo[l]};
+  return {P.level_begin[l], P.level_begin[l + 1] - P.level_begin[l]};
+}
+
+void upward_impl(fmm_plan_s& P, int64_t leaf_b, int64_t leaf_e, bool own = false) {
   cudaStream_t s = P.stream;
   const int nc = P.nc;
   if (leaf_e > leaf_b) {
@@ -570,21 +581,44 @@ void upward_impl(fmm_plan_s& P, int64_t leaf_b, int64_t leaf_e) {
       configured = sh;
     }
     for (int l = P.max_level - 1; l >= 0; --l) {
-      const int64_t lb = P.level_begin[l], le = P.level_begin[l + 1];
-      m2m_kernel<<<(unsigned)(le - lb), kM2MThreads, sh, s>>>(lb, P.cells.child, P.cells.nchild, P.cells.center, P.p,
-                                                              nc, P.M);
+      const LevelRange r = level_range(P, l, own);
+      if (r.n <= 0) continue;
+      m2m_kernel<<<(unsigned)r.n, kM2MThreads, sh, s>>>(r.b, P.cells.child, P.cells.nchild, P.cells.center, P.p, nc,
+                                                        P.M);
       FMM_LAUNCHED("m2m_kernel");
     }
     return;
   }
-  for (int l = P.max_level - 1; l >= 0; --l)
-    launch_shift<false>(P, P.level_begin[l], P.level_begin[l + 1] - P.level_begin[l]);
+  for (int l = P.max_level - 1; l >= 0; --l) {
+    const LevelRange r = level_range(P, l, own);
+    launch_shift<false>(P, r.b, r.n);
+  }
+}
+
+void downward_impl(fmm_plan_s& P, bool own) {
+  const int nc = P.nc;
+  if (P.shift_variant == 1) {
+    const size_t sh = sizeof(double2) * 9 * nc;
+    for (int l = 0; l < P.max_level; ++l) {
+      const LevelRange r = level_range(P, l, own);
+      if (r.n <= 0) continue;
+      l2l_kernel<<<(unsigned)r.n, kM2MThreads, sh, P.stream>>>(r.b, P.cells.child, P.cells.nchild, P.cells.center,
+                                                               P.p, nc, P.L);
+      FMM_LAUNCHED("l2l_kernel");
+    }
+    return;
+  }
+  for (int l = 0; l < P.max_level; ++l) {
+    const LevelRange r = level_range(P, l, own);
+    launch_shift<true>(P, r.b, r.n);
+  }
 }
 
 }  // namespace
 
 void upward(fmm_plan_s& P) { upward_impl(P, 0, P.nleaves); }
-void upward_own(fmm_plan_s& P) { upward_impl(P, P.own_leaf_begin, P.own_leaf_end); }
+// multi-GPU (LET): P2M of this rank's leaves, M2M of the cells overlapping its range
+void upward_own(fmm_plan_s& P) { upward_impl(P, P.own_leaf_begin, P.own_leaf_end, true); }
 
 void m2l_pass(fmm_plan_s& P) {
   const int nc = P.nc;
@@ -594,21 +628,9 @@ void m2l_pass(fmm_plan_s& P) {
   FMM_LAUNCHED("m2l_v1_kernel");
 }
 
-void downward(fmm_plan_s& P) {
-  const int nc = P.nc;
-  if (P.shift_variant == 1) {
-    const size_t sh = sizeof(double2) * 9 * nc;
-    for (int l = 0; l < P.max_level; ++l) {
-      const int64_t lb = P.level_begin[l], le = P.level_begin[l + 1];
-      l2l_kernel<<<(unsigned)(le - lb), kM2MThreads, sh, P.stream>>>(lb, P.cells.child, P.cells.nchild,
-                                                                     P.cells.center, P.p, nc, P.L);
-      FMM_LAUNCHED("l2l_kernel");
-    }
-    return;
-  }
-  for (int l = 0; l < P.max_level; ++l)
-    launch_shift<true>(P, P.level_begin[l], P.level_begin[l + 1] - P.level_begin[l]);
-}
+void downward(fmm_plan_s& P) { downward_impl(P, false); }
+// multi-GPU (LET): L2L of the cells overlapping this rank's range only
+void downward_own(fmm_plan_s& P) { downward_impl(P, true); }
 
 // the M2M and L2L operators A(+,+,+) in packed DMMA fragment order (shift_variant 2)
 void shift_setup(fmm_plan_s& P) {

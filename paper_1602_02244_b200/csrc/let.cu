@@ -9,15 +9,17 @@
 // boundaries. Per mat-vec (the caller moves the buffers with its collectives):
 //   1. q: each rank sends every charge of its caller slice to the owner of the
 //      particle and to every rank whose near field needs it (halo leaves);
-//   2. upward pass on the owned particles only: P2M of own leaves, M2M of every
-//      cell (cells outside the range stay exactly zero, so a cell straddling
-//      several ranks holds this rank's PARTIAL multipole, by linearity of M2M);
+//   2. upward pass on the owned particles only: P2M of own leaves, M2M of the cells
+//      overlapping the range (their children outside it read as zero, so a cell
+//      straddling several ranks holds this rank's PARTIAL multipole, by linearity
+//      of M2M);
 //   3. shared (straddling) cells: all partials are all-gathered and summed in
 //      rank order (deterministic); boundary multipoles: each rank sends the
 //      complete multipoles of its own cells that are M2L sources of another
 //      rank's targets;
-//   4. M2L for the targets overlapping the range, L2L, near field of own leaves
-//      (halo charges received in step 1), results in owned Morton order;
+//   4. M2L for the targets overlapping the range (a rank-local pair list), L2L of
+//      the cells overlapping it, near field of own leaves (halo charges received in
+//      step 1), results in owned Morton order;
 //   5. results are routed back to the callers' slices.
 // Index lists are built on the host at fmm_let_setup from the global tree; the
 // moves are gathers/scatters on the device. let_lists() is plain host code with
@@ -31,23 +33,52 @@
 namespace fmm {
 
 // ----------------------------------------------------------------------------- host
-// Owner range cuts: first leaf whose begin >= r * n / world, for r = 0..world.
-std::vector<int64_t> let_cuts(const int32_t* leaf_begin_sorted, int64_t nleaves, int64_t n, int world) {
+// Owner range cuts, cost-weighted (the Plummer tree is strongly non-uniform, so
+// equal particle counts are not equal work). Each target cell's work is spread evenly over its
+// particles: 11 flop per P2P interaction of a target leaf, kM2LCost per M2L pair of a target
+// cell (the pairs of an ancestor are shared by the leaves below it), plus a per-particle term
+// for P2M / L2P. Rank r's range starts at the first leaf boundary where the running weight
+// reaches r / world of the total, so ranges are contiguous in Morton order and never split a
+// leaf (one 3-D -> 1-D ordering serves locality and partitioning).
+std::vector<int64_t> let_cuts(int64_t n, int world, int p, const int32_t* cbeg, const int32_t* cend, int64_t nleaves,
+                              const int32_t* leaves /*sorted by begin*/, int64_t np2p, const int32_t* p2p_tgt,
+                              const int32_t* p2p_src, int64_t nm2l, const int32_t* m2l_tgt) {
+  std::vector<double> dens(n + 1, 0.0);  // difference array of per-particle cost density
+  auto spread = [&](int32_t c, double w) {
+    const int64_t a = cbeg[c], b = cend[c];
+    if (b <= a) return;
+    dens[a] += w / (double)(b - a);
+    dens[b] -= w / (double)(b - a);
+  };
+  const double m2l_cost = 6.0 * (p + 1.0) * (p + 1.0) * (p + 1.0);  // executed flops of one rotation-form pair
+  for (int64_t k = 0; k < np2p; ++k)
+    spread(p2p_tgt[k], 11.0 * (double)(cend[p2p_tgt[k]] - cbeg[p2p_tgt[k]]) * (cend[p2p_src[k]] - cbeg[p2p_src[k]]));
+  for (int64_t k = 0; k < nm2l; ++k) spread(m2l_tgt[k], m2l_cost);
+  const double per_particle = 18.0 * (p + 1.0) * (p + 2.0) / 2.0;  // P2M + L2P
+  std::vector<double> leafw(nleaves + 1, 0.0);  // prefix sums of leaf weights in Morton order
+  double run = 0.0;
+  int64_t pos = 0;
+  double acc = 0.0;
+  for (int64_t i = 0; i < nleaves; ++i) {
+    const int64_t a = cbeg[leaves[i]], b = cend[leaves[i]];
+    double w = 0.0;
+    for (; pos < a; ++pos) run += dens[pos];
+    for (; pos < b; ++pos) {
+      run += dens[pos];
+      w += run + per_particle;
+    }
+    acc += w;
+    leafw[i + 1] = acc;
+  }
   std::vector<int64_t> B(world + 1);
   for (int r = 0; r <= world; ++r) {
-    const int64_t target = (int64_t)r * n / world;
-    int64_t lo = 0, hi = nleaves;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) / 2;
-      if (leaf_begin_sorted[mid] < target)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    B[r] = lo < nleaves ? leaf_begin_sorted[lo] : n;
+    const double target = acc * r / world;
+    const int64_t i = std::lower_bound(leafw.begin(), leafw.end(), target) - leafw.begin();  // first prefix >= target
+    B[r] = i < nleaves ? cbeg[leaves[i]] : n;
   }
   B[0] = 0;
   B[world] = n;
+  for (int r = 1; r <= world; ++r) B[r] = std::max(B[r], B[r - 1]);
   return B;
 }
 
@@ -58,14 +89,13 @@ int find_rank(const std::vector<int64_t>& off, int64_t x) {  // off[r] <= x < of
 }  // namespace
 
 // All index lists of rank `me` (host arrays in, host vectors out). See fmm.h fmm_let_*.
-void let_lists(int64_t n, int world, int me, const int64_t* caller_off /*[world+1]*/, const uint32_t* perm,
+void let_lists(int64_t n, int world, int me, int p, const int64_t* caller_off /*[world+1]*/, const uint32_t* perm,
                int64_t ncells, const int32_t* cbeg, const int32_t* cend, int64_t nleaves,
                const int32_t* leaves /*sorted by begin*/, int64_t np2p, const int32_t* p2p_tgt,
                const int32_t* p2p_src, int64_t nm2l, const int32_t* m2l_tgt, const int32_t* m2l_src,
                LetLists& out) {
-  std::vector<int32_t> lbeg(nleaves);
-  for (int64_t i = 0; i < nleaves; ++i) lbeg[i] = cbeg[leaves[i]];
-  const std::vector<int64_t> B = let_cuts(lbeg.data(), nleaves, n, world);
+  const std::vector<int64_t> B =
+      let_cuts(n, world, p, cbeg, cend, nleaves, leaves, np2p, p2p_tgt, p2p_src, nm2l, m2l_tgt);
   const std::vector<int64_t> C(caller_off, caller_off + world + 1);
   out.world = world;
   out.rank_begin = B;
@@ -221,6 +251,13 @@ __global__ void sum_shared_kernel(const double* __restrict__ recv, const int32_t
   M[(int64_t)cells[k] * ncd + (e - k * ncd)] = v;
 }
 
+__global__ void zero_cells_kernel(const int32_t* __restrict__ cells, int64_t n, int ncd, double* __restrict__ M) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * ncd) return;
+  const int64_t k = e / ncd;
+  M[(int64_t)cells[k] * ncd + (e - k * ncd)] = 0.0;
+}
+
 template <typename T>
 void upload(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
   d.alloc((int64_t)h.size());
@@ -228,6 +265,53 @@ void upload(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
 }
 
 }  // namespace
+
+// host copies of the tree and lists the partition and the exchange lists are built from
+void let_host_copy(fmm_plan_s& P) {
+  LetHost& H = P.let_host;
+  if (H.valid) return;
+  cudaStream_t s = P.stream;
+  const int64_t nc = P.cells.n;
+  H.perm.resize(P.n);
+  H.cb.resize(nc);
+  H.ce.resize(nc);
+  H.child.resize(nc);
+  H.nchild.resize(nc);
+  H.lv.resize(P.nleaves);
+  H.pt.resize(P.p2p.n);
+  H.ps.resize(P.p2p.n);
+  H.mt.resize(P.m2l.n);
+  H.ms.resize(P.m2l.n);
+  auto d2h = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes) FMM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+  };
+  d2h(H.perm.data(), P.perm.ptr, sizeof(uint32_t) * P.n);
+  d2h(H.cb.data(), P.cells.begin.ptr, sizeof(int32_t) * nc);
+  d2h(H.ce.data(), P.cells.end.ptr, sizeof(int32_t) * nc);
+  d2h(H.child.data(), P.cells.child.ptr, sizeof(int32_t) * nc);
+  d2h(H.nchild.data(), P.cells.nchild.ptr, sizeof(int32_t) * nc);
+  d2h(H.lv.data(), P.leaves.ptr, sizeof(int32_t) * P.nleaves);
+  d2h(H.pt.data(), P.p2p.tgt.ptr, sizeof(int32_t) * P.p2p.n);
+  d2h(H.ps.data(), P.p2p.src.ptr, sizeof(int32_t) * P.p2p.n);
+  d2h(H.mt.data(), P.m2l.tgt.ptr, sizeof(int32_t) * P.m2l.n);
+  d2h(H.ms.data(), P.m2l.src.ptr, sizeof(int32_t) * P.m2l.n);
+  FMM_CUDA(cudaStreamSynchronize(s));
+  H.valid = true;
+}
+
+// this rank's Morton range (cost-weighted cut at leaf boundaries, let_cuts)
+void let_partition(fmm_plan_s& P) {
+  let_host_copy(P);
+  const LetHost& H = P.let_host;
+  const std::vector<int64_t> B = let_cuts(P.n, P.world, P.p, H.cb.data(), H.ce.data(), P.nleaves, H.lv.data(), P.p2p.n,
+                                          H.pt.data(), H.ps.data(), P.m2l.n, H.mt.data());
+  P.own_begin = B[P.rank];
+  P.own_end = B[P.rank + 1];
+  P.own_leaf_begin = std::lower_bound(H.lv.begin(), H.lv.end(), P.own_begin,
+                                      [&](int32_t l, int64_t v) { return H.cb[l] < v; }) - H.lv.begin();
+  P.own_leaf_end = std::lower_bound(H.lv.begin(), H.lv.end(), P.own_end,
+                                    [&](int32_t l, int64_t v) { return H.cb[l] < v; }) - H.lv.begin();
+}
 
 void let_setup(fmm_plan_s& P, const int64_t* caller_counts) {
   cudaStream_t s = P.stream;
@@ -237,25 +321,13 @@ void let_setup(fmm_plan_s& P, const int64_t* caller_counts) {
     C[r + 1] = C[r] + caller_counts[r];
   }
   if (C[P.world] != P.n) throw Error(FMM_ERR_USAGE, "fmm_let_setup: caller counts do not sum to n");
+  let_host_copy(P);
+  const LetHost& H = P.let_host;
   const int64_t nc = P.cells.n;
-  std::vector<uint32_t> perm(P.n);
-  std::vector<int32_t> cb(nc), ce(nc), lv(P.nleaves), pt(P.p2p.n), ps(P.p2p.n), mt(P.m2l.n), ms(P.m2l.n);
-  auto d2h = [&](void* dst, const void* src, size_t bytes) {
-    if (bytes) FMM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
-  };
-  d2h(perm.data(), P.perm.ptr, sizeof(uint32_t) * P.n);
-  d2h(cb.data(), P.cells.begin.ptr, sizeof(int32_t) * nc);
-  d2h(ce.data(), P.cells.end.ptr, sizeof(int32_t) * nc);
-  d2h(lv.data(), P.leaves.ptr, sizeof(int32_t) * P.nleaves);
-  d2h(pt.data(), P.p2p.tgt.ptr, sizeof(int32_t) * P.p2p.n);
-  d2h(ps.data(), P.p2p.src.ptr, sizeof(int32_t) * P.p2p.n);
-  d2h(mt.data(), P.m2l.tgt.ptr, sizeof(int32_t) * P.m2l.n);
-  d2h(ms.data(), P.m2l.src.ptr, sizeof(int32_t) * P.m2l.n);
-  FMM_CUDA(cudaStreamSynchronize(s));
   LetLists& L = P.let;
-  let_lists(P.n, P.world, P.rank, C.data(), perm.data(), nc, cb.data(), ce.data(), P.nleaves, lv.data(), P.p2p.n,
-            pt.data(), ps.data(), P.m2l.n, mt.data(), ms.data(), L);
-  // this rank's range must be the one choose_own_range picked (same cut rule)
+  let_lists(P.n, P.world, P.rank, P.p, C.data(), H.perm.data(), nc, H.cb.data(), H.ce.data(), P.nleaves,
+            H.lv.data(), P.p2p.n, H.pt.data(), H.ps.data(), P.m2l.n, H.mt.data(), H.ms.data(), L);
+  // this rank's range must be the one let_partition picked (same cut rule)
   if (L.rank_begin[P.rank] != P.own_begin || L.rank_begin[P.rank + 1] != P.own_end)
     throw Error(FMM_ERR_CUDA, "fmm_let_setup: owner range mismatch");
   upload(P.let_dev.q_send_rows, L.q_send_rows, s);
@@ -271,7 +343,44 @@ void let_setup(fmm_plan_s& P, const int64_t* caller_counts) {
   upload(P.let_dev.shared32, sh32, s);
   P.let_dev.phi_own.alloc(std::max<int64_t>(1, P.own_end - P.own_begin));
   P.let_dev.grad_own.alloc(std::max<int64_t>(1, 3 * (P.own_end - P.own_begin)));
+  // ---- the rank-local passes (only what this rank's targets need):
+  // per level, the cells overlapping the owned range (contiguous: cells of a level are in
+  // Morton order); children of those that lie outside it, and shared cells that lie outside
+  // it, hold zero multipoles (M2M inputs, this rank's partials); M2L pairs whose target
+  // overlaps the range
+  const int64_t ob = P.own_begin, oe = P.own_end;
+  auto overlaps = [&](int64_t c) { return H.ce[c] > ob && H.cb[c] < oe && H.ce[c] > H.cb[c]; };
+  P.let_level_lo.assign(P.max_level + 1, 0);
+  P.let_level_hi.assign(P.max_level + 1, 0);
+  std::vector<int32_t> zero;
+  for (int l = 0; l <= P.max_level; ++l) {
+    int64_t lo = P.level_begin[l + 1], hi = P.level_begin[l];
+    for (int64_t c = P.level_begin[l]; c < P.level_begin[l + 1]; ++c)
+      if (overlaps(c)) {
+        lo = std::min(lo, c);
+        hi = std::max(hi, c + 1);
+      }
+    if (hi <= lo) lo = hi = P.level_begin[l];
+    P.let_level_lo[l] = lo;
+    P.let_level_hi[l] = hi;
+    for (int64_t c = lo; c < hi; ++c)
+      for (int k = 0; k < H.nchild[c]; ++k)
+        if (!overlaps(H.child[c] + k)) zero.push_back(H.child[c] + k);
+  }
+  for (int32_t c : L.shared)  // a straddling cell away from this range: this rank's partial is 0
+    if (!overlaps(c)) zero.push_back(c);
+  upload(P.let_dev.zero_cells, zero, s);
+  std::vector<int32_t> ot, os;
+  for (int64_t k = 0; k < P.m2l.n; ++k)
+    if (overlaps(H.mt[k])) {
+      ot.push_back(H.mt[k]);
+      os.push_back(H.ms[k]);
+    }
+  upload(P.let_dev.m2l_tgt, ot, s);
+  upload(P.let_dev.m2l_src, os, s);
+  if (P.m2l_variant == 4) m2l_v4_resize(P, (int64_t)ot.size());
   P.let_ready = true;
+  P.let_host = LetHost{};  // the host copies are no longer needed
   FMM_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -301,7 +410,12 @@ void let_upward(fmm_plan_s& P, const double* q_recv, double* shared_send, double
     scatter_q_kernel<<<cdiv(n, 256), 256, 0, s>>>(q_recv, P.let_dev.q_recv_pos.ptr, n, P.pos, P.flags);
     FMM_LAUNCHED("scatter_q_kernel");
   }
-  FMM_CUDA(cudaMemsetAsync(P.M.ptr, 0, sizeof(double2) * P.M.count, s));  // cells outside the range stay 0
+  const int64_t nz = P.let_dev.zero_cells.count;  // children outside the range of cells inside it
+  if (nz > 0) {
+    zero_cells_kernel<<<cdiv(nz * 2 * P.nc, 256), 256, 0, s>>>(P.let_dev.zero_cells.ptr, nz, 2 * P.nc,
+                                                                (double*)P.M.ptr);
+    FMM_LAUNCHED("zero_cells_kernel");
+  }
   upward_own(P);
   gather((const double*)P.M.ptr, P.let_dev.shared, 2 * P.nc, shared_send, s);
   gather((const double*)P.M.ptr, P.let_dev.m_send_cells, 2 * P.nc, m_send, s);

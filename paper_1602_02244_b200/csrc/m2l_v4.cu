@@ -628,7 +628,7 @@ __global__ void m2l4_mtilde_kernel(const double2* __restrict__ M, const double4*
 // launch geometry (setup): warps per CTA from shared memory and registers, units sized so every
 // warp gets the same number of units (as close to kUnitChunks chunks as that allows)
 template <int P>
-void size_v4(fmm_plan_s& P_) {
+void size_v4(fmm_plan_s& P_, int64_t npairs) {
   using G = V4Geo<P>;
   M2L4& V = P_.m2l4;
   const size_t sh = (size_t)32 * G::NRS * sizeof(double);
@@ -641,7 +641,7 @@ void size_v4(fmm_plan_s& P_) {
   const int fit = std::max(1, std::min({by_smem, by_regs, kMaxWarpsPerCta}));
   V.wpc = std::max(1, std::min(V.warps_per_sm > 0 ? V.warps_per_sm : fit, fit));
   V.smem = sh * V.wpc;
-  const int64_t nchunks = (P_.m2l.n + 31) / 32, warps = (int64_t)nsm * V.wpc;
+  const int64_t nchunks = (npairs + 31) / 32, warps = (int64_t)nsm * V.wpc;
   V.uchunks = V.unit_chunks;
   if (V.uchunks <= 0) {
     const int64_t rounds = std::max<int64_t>(1, (nchunks + warps * kUnitChunks - 1) / (warps * kUnitChunks));
@@ -664,29 +664,29 @@ void launch_v4(fmm_plan_s& P_, const V4Args& a) {
 }
 
 template <int P>
-void dispatch_v4(fmm_plan_s& P_, const V4Args* a) {  // a == nullptr: size at setup
+void dispatch_v4(fmm_plan_s& P_, const V4Args* a, int64_t npairs) {  // a == nullptr: size at setup
   if (a)
     launch_v4<P>(P_, *a);
   else
-    size_v4<P>(P_);
+    size_v4<P>(P_, npairs);
 }
 
-void v4_switch(fmm_plan_s& P, const V4Args* a) {
+void v4_switch(fmm_plan_s& P, const V4Args* a, int64_t npairs = 0) {
   switch (P.p) {
 #ifdef FMM_V4_ONLY  // development builds: one instantiation (compile time)
-    case FMM_V4_ONLY: dispatch_v4<FMM_V4_ONLY>(P, a); break;
+    case FMM_V4_ONLY: dispatch_v4<FMM_V4_ONLY>(P, a, npairs); break;
 #else
-    case 2: dispatch_v4<2>(P, a); break;
-    case 3: dispatch_v4<3>(P, a); break;
-    case 4: dispatch_v4<4>(P, a); break;
-    case 5: dispatch_v4<5>(P, a); break;
-    case 6: dispatch_v4<6>(P, a); break;
-    case 7: dispatch_v4<7>(P, a); break;
-    case 8: dispatch_v4<8>(P, a); break;
-    case 9: dispatch_v4<9>(P, a); break;
-    case 10: dispatch_v4<10>(P, a); break;
-    case 11: dispatch_v4<11>(P, a); break;
-    case 12: dispatch_v4<12>(P, a); break;
+    case 2: dispatch_v4<2>(P, a, npairs); break;
+    case 3: dispatch_v4<3>(P, a, npairs); break;
+    case 4: dispatch_v4<4>(P, a, npairs); break;
+    case 5: dispatch_v4<5>(P, a, npairs); break;
+    case 6: dispatch_v4<6>(P, a, npairs); break;
+    case 7: dispatch_v4<7>(P, a, npairs); break;
+    case 8: dispatch_v4<8>(P, a, npairs); break;
+    case 9: dispatch_v4<9>(P, a, npairs); break;
+    case 10: dispatch_v4<10>(P, a, npairs); break;
+    case 11: dispatch_v4<11>(P, a, npairs); break;
+    case 12: dispatch_v4<12>(P, a, npairs); break;
 #endif
     default: throw Error(FMM_ERR_USAGE, "m2l v4: order out of range");
   }
@@ -714,8 +714,14 @@ void m2l_v4_setup(fmm_plan_s& P) {
   const char* uc = getenv("FMM_V4_UNIT_CHUNKS");  // tests: small units cross many targets
   V.unit_chunks = uc ? atoi(uc) : 0;
   V.nunits = 0;
-  if (P.m2l.n > 0) v4_switch(P, nullptr);
+  if (P.m2l.n > 0) v4_switch(P, nullptr, P.m2l.n);
   FMM_CUDA(cudaStreamSynchronize(P.stream));
+}
+
+// multi-GPU (LET): units over the rank-local pair list (targets overlapping the owned range)
+void m2l_v4_resize(fmm_plan_s& P, int64_t npairs) {
+  P.m2l4.nunits = 0;
+  if (npairs > 0) v4_switch(P, nullptr, npairs);
 }
 
 void m2l_v4_pass(fmm_plan_s& P) {
@@ -728,9 +734,10 @@ void m2l_v4_pass(fmm_plan_s& P) {
                                                            V.ihalf);
   FMM_LAUNCHED("m2l4_mtilde_kernel");
   V4Args a;
-  a.tgt = P.m2l.tgt;
-  a.src = P.m2l.src;
-  a.npairs = P.m2l.n;
+  const bool own = P.let_ready;  // LET: the pairs of targets overlapping the owned range
+  a.tgt = own ? P.let_dev.m2l_tgt.ptr : P.m2l.tgt.ptr;
+  a.src = own ? P.let_dev.m2l_src.ptr : P.m2l.src.ptr;
+  a.npairs = own ? P.let_dev.m2l_tgt.count : P.m2l.n;
   a.nunits = V.nunits;
   a.uchunks = V.uchunks;
   a.center = P.cells.center;

@@ -133,10 +133,23 @@ struct LetDev {
   DevBuf<int64_t> q_send_rows, q_recv_pos, shared, m_send_cells, m_recv_cells, phi_send_idx, phi_recv_rows;
   DevBuf<int32_t> shared32;
   DevBuf<double> phi_own, grad_own;  // owned results in Morton order
+  DevBuf<int32_t> zero_cells;        // children outside the owned range of cells overlapping it (M = 0)
+  DevBuf<int32_t> m2l_tgt, m2l_src;  // M2L pairs whose target overlaps the owned range (grouped by target)
+  // collective mode (fmm_exec.nccl_id): the exchange buffers fmm_matvec moves with NCCL
+  DevBuf<double> q_send, q_recv, shared_send, shared_recv, m_send, m_recv, phi_send, phi_recv, grad_send, grad_recv;
   int64_t bytes() const {
     return q_send_rows.bytes() + q_recv_pos.bytes() + shared.bytes() + m_send_cells.bytes() + m_recv_cells.bytes() +
-           phi_send_idx.bytes() + phi_recv_rows.bytes() + shared32.bytes() + phi_own.bytes() + grad_own.bytes();
+           phi_send_idx.bytes() + phi_recv_rows.bytes() + shared32.bytes() + phi_own.bytes() + grad_own.bytes() +
+           zero_cells.bytes() + m2l_tgt.bytes() + m2l_src.bytes() + q_send.bytes() + q_recv.bytes() +
+           shared_send.bytes() + shared_recv.bytes() + m_send.bytes() + m_recv.bytes() + phi_send.bytes() +
+           phi_recv.bytes() + grad_send.bytes() + grad_recv.bytes();
   }
+};
+// host copies of the tree and lists while the partition and the exchange lists are built (setup)
+struct LetHost {
+  bool valid = false;
+  std::vector<uint32_t> perm;
+  std::vector<int32_t> cb, ce, child, nchild, lv, pt, ps, mt, ms;
 };
 
 }  // namespace fmm
@@ -199,7 +212,15 @@ struct fmm_plan_s {
   // multi-GPU LET exchange (let.cu)
   fmm::LetLists let;
   fmm::LetDev let_dev;
+  fmm::LetHost let_host;
+  std::vector<int64_t> let_level_lo, let_level_hi;  // per level: cells overlapping the owned range
   bool let_ready = false;
+  // collective mode (world > 1 with fmm_exec.nccl_id): callers pass local slices, libfmm moves
+  // the LET buffers with NCCL (comm.cu)
+  void* nccl_comm = nullptr;  // ncclComm_t
+  bool collective = false;
+  int64_t n_local = 0;
+  std::vector<int64_t> caller_counts;
   bool near_compact_out = false;  // near field writes owned results in Morton order (LET)
   // near field fused into the M2L v3 kernel (P2P by extra warps, then tail + L2P kernels)
   bool fuse_near = false;  // FMM_FUSE_NEAR=1: measured slower (profiles/r1_v3.md)
@@ -246,8 +267,23 @@ void near_pass_warp(fmm_plan_s& P, double* phi, double* grad);
 void near_fused_prepare(fmm_plan_s& P, bool grad);
 void near_fused_finish(fmm_plan_s& P, double* phi, double* grad);
 void gather_charges(fmm_plan_s& P, const double* q);
-std::vector<int64_t> let_cuts(const int32_t* leaf_begin_sorted, int64_t nleaves, int64_t n, int world);
-void let_lists(int64_t n, int world, int me, const int64_t* caller_off, const uint32_t* perm, int64_t ncells,
+std::vector<int64_t> let_cuts(int64_t n, int world, int p, const int32_t* cbeg, const int32_t* cend, int64_t nleaves,
+                              const int32_t* leaves, int64_t np2p, const int32_t* p2p_tgt, const int32_t* p2p_src,
+                              int64_t nm2l, const int32_t* m2l_tgt);
+void let_host_copy(fmm_plan_s& P);
+void let_partition(fmm_plan_s& P);
+void m2l_v4_resize(fmm_plan_s& P, int64_t npairs);
+void downward_own(fmm_plan_s& P);
+// NCCL (comm.cu)
+void comm_unique_id(void* out);
+void comm_init(fmm_plan_s& P, const void* id);
+void comm_destroy(fmm_plan_s& P);
+std::vector<int64_t> comm_gather_counts(fmm_plan_s& P, int64_t n_local);
+void comm_gather_points(fmm_plan_s& P, const double* xyz_local, const std::vector<int64_t>& counts, DevBuf<double>& xyz);
+void comm_exchange(fmm_plan_s& P, const double* send, const std::vector<int64_t>& scount, double* recv,
+                   const std::vector<int64_t>& rcount, int width);
+void comm_allgather(fmm_plan_s& P, const double* send, int64_t count, double* recv);
+void let_lists(int64_t n, int world, int me, int p, const int64_t* caller_off, const uint32_t* perm, int64_t ncells,
                const int32_t* cbeg, const int32_t* cend, int64_t nleaves, const int32_t* leaves, int64_t np2p,
                const int32_t* p2p_tgt, const int32_t* p2p_src, int64_t nm2l, const int32_t* m2l_tgt,
                const int32_t* m2l_src, LetLists& out);

@@ -4,9 +4,11 @@ Design (north_star "Morton-ordered domain decomposition, with a
 local-essential-tree exchange (boundary multipoles plus halo particles) over
 NCCL/NVLink"): every rank builds the same global tree and lists
 from the all-gathered points (so the approximation is the single-GPU one,
-reading R12) and owns a contiguous Morton range of leaves. Per mat-vec the
-library (include/fmm.h fmm_let_*) packs and unpacks device buffers and this
-module moves them:
+reading R12) and owns a contiguous Morton range of leaves (cut by estimated
+work). Over NCCL the library itself runs everything (collective mode,
+include/fmm.h fmm_exec.nccl_id): this module only broadcasts the ncclUniqueId.
+Over other backends (gloo: the CPU tests) the library (fmm_let_*) packs and
+unpacks device buffers and this module moves them:
 
     Q      all-to-all-v   charges to their owner and to the ranks whose near
                           field needs them (halo leaves)
@@ -110,6 +112,23 @@ class DistributedPlan:
         self.world = dist.get_world_size(group)
         self.counts = gather_counts(points_local.shape[0], points_local.device, group)
         self.n = sum(self.counts)
+        self.collective = False
+        if plan_factory is None and self.world > 1 and _is_nccl(group):
+            # collective mode (include/fmm.h fmm_exec.nccl_id): libfmm gathers the points, builds
+            # the global tree and moves the whole exchange with NCCL on the plan's stream; this
+            # layer only hands it the ncclUniqueId (rank 0 makes it, the group broadcasts it)
+            from .fmm import Plan, nccl_unique_id
+
+            idt = torch.zeros(128, dtype=torch.uint8, device=points_local.device)
+            if self.rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+            self.plan = Plan(points_local, p, ncrit, theta, rank=self.rank, world=self.world,
+                             nccl_id=bytes(idt.cpu().numpy().tobytes()))
+            self.collective = True
+            self.let = None
+            self._buf = {}
+            return
         xyz = gather_rows(points_local, self.counts, group)
         if plan_factory is None:
             from .fmm import Plan
@@ -125,7 +144,7 @@ class DistributedPlan:
         return self._buf[grad]
 
     def matvec(self, q_local: torch.Tensor, grad: bool = False):
-        if self.world == 1:
+        if self.world == 1 or self.collective:
             return self.plan.matvec(q_local, grad=grad)
         L, pl, g = self.let, self.plan, self.group
         B = self._buffers(grad)

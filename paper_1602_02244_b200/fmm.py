@@ -15,11 +15,19 @@ import torch
 from . import _native as N
 
 
-def _exec(device: torch.device, stream=None, rank: int = 0, world: int = 1) -> N.FmmExec:
+def _exec(device: torch.device, stream=None, rank: int = 0, world: int = 1, nccl_id=None) -> N.FmmExec:
     if stream is None:
         stream = torch.cuda.current_stream(device)
     return N.FmmExec(device.index if device.index is not None else torch.cuda.current_device(),
-                     C.c_void_p(stream.cuda_stream), rank, world)
+                     C.c_void_p(stream.cuda_stream), rank, world,
+                     C.cast(nccl_id, C.c_void_p) if nccl_id is not None else None)
+
+
+def nccl_unique_id() -> bytes:
+    """A new ncclUniqueId (fmm_nccl_unique_id): make it on one rank, send it to the others."""
+    buf = C.create_string_buffer(128)
+    N.check(N.lib().fmm_nccl_unique_id(buf))
+    return buf.raw
 
 
 def _dev_f64(t: torch.Tensor, name: str, shape_tail=()) -> torch.Tensor:
@@ -39,14 +47,17 @@ class Plan:
     _dim = 3
 
     def __init__(self, points: torch.Tensor, p: int, ncrit: int, theta: float, *, rank: int = 0,
-                 world: int = 1, stream=None):
+                 world: int = 1, stream=None, nccl_id: bytes | None = None):
+        """nccl_id (world > 1): collective mode — ``points`` is this rank's slice, ``matvec``
+        takes and returns this rank's slices (include/fmm.h fmm_exec.nccl_id)."""
         points = _dev_f64(points, "points", (self._dim,))
         self.device = points.device
         self.n = points.shape[0]
         self.p, self.ncrit, self.theta = p, ncrit, theta
         self.rank, self.world = rank, world
         self._stream = stream
-        self._ex = _exec(self.device, stream, rank, world)
+        self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        self._ex = _exec(self.device, stream, rank, world, self._nccl_id)
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             setup = N.lib().fmm_setup if self._dim == 3 else N.lib().fmm_setup_2d
@@ -193,7 +204,7 @@ def direct(src: torch.Tensor, q: torch.Tensor, tgt: torch.Tensor | None = None, 
     return (phi, g) if grad else phi
 
 
-def let_lists_host(n, world, me, caller_off, perm, cbeg, cend, leaves, p2p, m2l, what):
+def let_lists_host(n, world, me, caller_off, perm, cbeg, cend, leaves, p2p, m2l, what, p=4):
     """Host-only exchange-list builder (fmm_let_lists_host; no device work): numpy arrays in, one list out."""
     import numpy as _np
 
@@ -205,7 +216,7 @@ def let_lists_host(n, world, me, caller_off, perm, cbeg, cend, leaves, p2p, m2l,
     pt, ps = a(p2p[:, 0], _np.int32), a(p2p[:, 1], _np.int32)
     mt, ms = a(m2l[:, 0], _np.int32), a(m2l[:, 1], _np.int32)
     ptr = lambda x: C.c_void_p(x.ctypes.data)  # noqa: E731
-    args = [int(n), int(world), int(me), ptr(co), ptr(pm), len(cb), ptr(cb), ptr(ce), len(lv), ptr(lv), len(pt),
+    args = [int(n), int(world), int(me), int(p), ptr(co), ptr(pm), len(cb), ptr(cb), ptr(ce), len(lv), ptr(lv), len(pt),
             ptr(pt), ptr(ps), len(mt), ptr(mt), ptr(ms), int(what)]
     cnt = C.c_int64()
     N.check(N.lib().fmm_let_lists_host(*args, None, 0, C.byref(cnt)))

@@ -29,6 +29,7 @@ class Tree:
     """Oracle tree + lists in the form the LET host code takes."""
 
     def __init__(self, x, p, ncrit, theta):
+        self.p = p
         orc = O.Plan(x, p, ncrit, theta)
         c = orc.cells()
         self.n = x.shape[0]
@@ -42,7 +43,7 @@ class Tree:
 
     def lists(self, world, me, caller_off, what):
         return let_lists_host(self.n, world, me, caller_off, self.perm, self.cbeg, self.cend, self.leaves,
-                              self.p2p, self.m2l, what)
+                              self.p2p, self.m2l, what, p=self.p)
 
 
 def caller_offsets(n, counts):
@@ -304,3 +305,72 @@ def test_let_matvec_matches_single_gpu_and_oracle(dist_name, n, p, ncrit, theta,
     if grad:
         g = torch.cat([r[1] for r in res]).cpu().numpy()
         assert O.rel_l2(g, single[1].cpu().numpy()) <= 1e-13
+
+
+# ------------------------------------------------------------ owner cuts
+def test_owner_cuts_balance_the_work():
+    """Cost-weighted cuts (let.cu let_cuts): on a Plummer tree, the work each
+    rank's targets carry — 11 flop per P2P interaction of its leaves plus the M2L pairs of the
+    cells overlapping its range — is within 25 % of the mean for 4 ranks, where equal particle
+    counts are not (the dense core has more interactions per particle)."""
+    x, _ = F.make("plummer", 40000)
+    T = Tree(x, 6, 32, 0.5)
+    W = 4
+    co = caller_offsets(T.n, (T.n // W,) * (W - 1) + (T.n - (W - 1) * (T.n // W),))
+    B = T.lists(W, 0, co, N.FMM_LET_RANK_BEGIN)
+    m2l_cost = 6.0 * 7**3
+
+    def work(B):
+        w = np.zeros(W)
+        own = lambda s: np.searchsorted(B, s, side="right") - 1  # noqa: E731
+        sz = (T.cend - T.cbeg).astype(np.float64)
+        for t, s in T.p2p:
+            w[own(T.cbeg[t])] += 11.0 * sz[t] * sz[s]
+        for t, _s in T.m2l:
+            for r in range(own(T.cbeg[t]), own(T.cend[t] - 1) + 1):
+                w[r] += m2l_cost
+        return w
+
+    wb = work(np.asarray(B))
+    assert wb.max() / wb.mean() <= 1.25, wb
+    counts = np.asarray([0] + [np.searchsorted(T.cbeg[T.leaves], r * T.n // W) for r in range(1, W)] + [len(T.leaves)])
+    Bc = np.array([T.cbeg[T.leaves][i] if i < len(T.leaves) else T.n for i in counts])
+    wc = work(Bc)
+    assert wb.max() / wb.mean() < wc.max() / wc.mean()
+
+
+# ------------------------------------------------------------ GPU: collective mode (NCCL inside libfmm)
+@pytest.mark.gpu
+@pytest.mark.parametrize("dist_name,n,p,ncrit,theta,grad", [
+    ("plummer", 30000, 8, 64, 0.5, True), ("cube", 20000, 10, 64, 0.4, False), ("sphere", 20000, 12, 128, 0.4, False),
+    ("plummer", 8000, 3, 16, 0.4, True)])
+def test_collective_mode_one_rank(dist_name, n, p, ncrit, theta, grad):
+    """fmm_exec.nccl_id (include/fmm.h): the collective setup (NCCL all-gather of counts and points,
+    cost-weighted partition, exchange lists and buffers) and the collective mat-vec (charges, shared
+    and boundary multipoles, results moved by NCCL on the plan's stream, rank-local M2M / M2L / L2L)
+    on a one-rank communicator — every step of the multi-GPU path but the peer transfers — match the
+    single-GPU plan and the oracle."""
+    from paper_1602_02244_b200 import Plan
+    from paper_1602_02244_b200.fmm import nccl_unique_id
+
+    x, q = F.make(dist_name, n)
+    dev = torch.device("cuda:0")
+    xd, qd = torch.from_numpy(x).to(dev), torch.from_numpy(q).to(dev)
+    uid = nccl_unique_id()
+    assert len(uid) == 128
+    pl = Plan(xd, p, ncrit, theta, rank=0, world=1, nccl_id=uid)
+    out = pl.matvec(qd, grad=grad)
+    single = Plan(xd, p, ncrit, theta).matvec(qd, grad=grad)
+    torch.cuda.synchronize()
+    pl.sync()
+    phi = (out[0] if grad else out).cpu().numpy()
+    ref = (single[0] if grad else single).cpu().numpy()
+    assert O.rel_l2(phi, ref) <= 1e-14
+    if grad:
+        assert O.rel_l2(out[1].cpu().numpy(), single[1].cpu().numpy()) <= 1e-14
+    po = O.fmm(x, q, p, ncrit, theta, nthreads=O.default_threads())
+    assert O.rel_l2(phi, po) <= 1e-11
+    st = pl.stats()
+    assert st["own_begin"] == 0 and st["own_end"] == n and st["bytes_by"]["let"] > 0
+    ph = pl.matvec_host(q)  # the end-to-end entry point in collective mode
+    assert O.rel_l2(ph.numpy(), phi) <= 1e-15

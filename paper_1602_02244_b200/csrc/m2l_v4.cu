@@ -59,6 +59,7 @@ constexpr int kMinP = 2, kMaxP4 = 12;  // orders served by v4 (others: v3 / v2)
 constexpr int kUnitChunks = 16;        // default chunks of 32 pairs per work unit (balanced at launch)
 constexpr int kMaxWarpsPerCta = 8;     // M2L v4 CTA: up to 8 one-warp workers
 
+
 __host__ __device__ constexpr int nnzF(int n) { return n * n + n + 1; }
 __host__ __device__ constexpr int offF(int n) {
   int s = 0;
@@ -490,13 +491,20 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
     double acc[KPL];
 #pragma unroll
     for (int c = 0; c < KPL; ++c) acc[c] = 0.0;
+    // the chunk's (target, source) pairs, loaded one chunk ahead (their latency off the critical path)
+    int tg_next = lane < u1 - u0 ? a.tgt[u0 + lane] : -1, sr_next = lane < u1 - u0 ? a.src[u0 + lane] : 0;
     for (int ich = 0; ich < a.uchunks; ++ich) {
       const int64_t base = u0 + 32 * ich;
       const int nact = (int)max((int64_t)0, min((int64_t)32, u1 - base));
       const bool act = lane < nact;
-      const int tg = act ? a.tgt[base + lane] : -1;
-      const int sr = act ? a.src[base + lane] : 0;
+      const int tg = tg_next, sr = sr_next;
+      {
+        const int64_t nb = base + 32 + lane;
+        tg_next = nb < u1 ? a.tgt[nb] : -1;
+        sr_next = nb < u1 ? a.src[nb] : 0;
+      }
       // 1. source rows into the lanes' buffers (coalesced: row by row)
+#pragma unroll 4
       for (int l = 0; l < nact; ++l) {
         const int s = __shfl_sync(0xffffffffu, sr, l);
         const double* g = a.Mt + (int64_t)s * NR;

@@ -76,3 +76,20 @@ def test_product_does_not_import_oracle():
         for f in fs:
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 assert not pat.search(open(os.path.join(dp, f)).read()), f
+
+
+def test_m2l_v4_constants_stay_uniform():
+    """M2L v4 (csrc/m2l_v4.cu) reads its fixed operator as warp-uniform constant-bank loads (LDCU into
+    uniform registers, DFMA operands) once per use: no per-thread LDC (the ADU pipe throttled an
+    earlier build to 5 TFLOP/s), no spills, one copy of the pair code. A compiler-level property of
+    the built library, checked in its SASS."""
+    out = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_1602_02244_b200", "libfmm.so")],
+                         capture_output=True, text=True).stdout
+    funcs = re.split(r"\n\s+Function : ", out)
+    body = [f for f in funcs if f.startswith("_ZN3fmm") and "m2l_v4_kernelILi10E" in f.split("\n")[0]]
+    assert len(body) == 1
+    sass = body[0]
+    assert len(re.findall(r"\bLDC(?:\.64)?\s+R\d+, c\[0x3\]", sass)) == 0
+    assert len(re.findall(r"\bLDCU(?:\.64|\.128)?\s+UR\d+, c\[0x3\]", sass)) > 1000
+    assert len(re.findall(r"\bDFMA\b", sass)) < 4000  # one copy of the ~3.2K-FMA pair code
+    assert "STL" not in sass  # no register spills

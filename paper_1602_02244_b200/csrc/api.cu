@@ -131,6 +131,49 @@ void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
     }
     return;
   }
+  if (P.overlap_near && P.near_variant == 2 && !P.fuse_near) {
+    // near field overlapped with the far field: the P2P sums need only the
+    // charges, the far field (M2L, L2L) only the multipoles. After the upward pass both are
+    // released together, the far field on a high-priority stream (its persistent M2L CTAs are
+    // placed first, one per SM) and the P2P on a low-priority one filling the SMs' remaining
+    // room; L2P + rescale + scatter on the caller's stream once both are done.
+    cudaStream_t sF = P.stream2, sN = P.stream3, s0 = P.stream;
+    FMM_CUDA(cudaEventRecord(P.ev_q, s0));
+    FMM_CUDA(cudaStreamWaitEvent(sF, P.ev_q, 0));
+    P.stream = sF;  // the far-field stages enqueue on P.stream
+    fmm::upward(P);
+    FMM_CUDA(cudaEventRecord(P.ev_up, sF));
+    FMM_CUDA(cudaStreamWaitEvent(sN, P.ev_up, 0));
+    P.stream = sN;
+    fmm::near_p2p_async(P, grad != nullptr, sN);
+    FMM_CUDA(cudaEventRecord(P.ev_p2p, sN));
+    P.stream = sF;
+    if (T.on) FMM_CUDA(cudaEventRecord(P.ev[1], sF));
+    if (P.m2l_variant == 4)
+      fmm::m2l_v4_pass(P);
+    else if (P.m2l_variant >= 2)
+      fmm::m2l_dmma_pass(P);
+    else
+      fmm::m2l_pass(P);
+    if (T.on) FMM_CUDA(cudaEventRecord(P.ev[2], sF));
+    fmm::downward(P);
+    FMM_CUDA(cudaEventRecord(P.ev_far, sF));
+    P.stream = s0;
+    FMM_CUDA(cudaStreamWaitEvent(s0, P.ev_far, 0));
+    FMM_CUDA(cudaStreamWaitEvent(s0, P.ev_p2p, 0));
+    T.mark(3);
+    fmm::near_l2p_out(P, phi, grad);
+    T.mark(4);
+    if (T.on) {  // (M2L concurrent with the P2P; NEAR = the L2P tail; UPWARD = up to the M2L start)
+      FMM_CUDA(cudaEventSynchronize(P.ev[4]));
+      P.t_matvec[FMM_T_UPWARD] = T.between(0, 1);
+      P.t_matvec[FMM_T_M2L] = T.between(1, 2);
+      P.t_matvec[FMM_T_DOWNWARD] = T.between(2, 3);
+      P.t_matvec[FMM_T_NEAR] = T.between(3, 4);
+      P.t_matvec[FMM_T_MATVEC_TOTAL] = T.between(0, 4);
+    }
+    return;
+  }
   fmm::upward(P);
   // near field fused into the M2L v3 kernel (P2P warps on the FP64 pipe)
   P.near_fused_active = P.fuse_near && P.m2l_variant == 3 && P.near_variant == 2 && P.m2l_dmma.ntiles > 0;
@@ -282,6 +325,19 @@ extern "C" {
 }  // extern "C"
 
 namespace {
+// streams, events and the NCCL communicator of a plan, then the plan (device buffers: DevBuf)
+void release_plan(fmm_plan_s* P) {
+  for (cudaStream_t st : {P->stream2, P->stream3})
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t e : {P->ev_q, P->ev_up, P->ev_p2p, P->ev_far})
+    if (e) cudaEventDestroy(e);
+  try {
+    fmm::comm_destroy(*P);
+  } catch (...) {
+  }
+  delete P;
+}
+
 fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int ncrit, double theta,
                       const fmm_exec* ex, int dim) {
   if (!out) return fail(FMM_ERR_USAGE, "fmm_setup: out is NULL");
@@ -349,6 +405,16 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
     const char* dbg = getenv("FMM_DEBUG_SKIP_L2L");  // export M2L-only local expansions
     P->debug_skip_l2l = dbg && dbg[0] == '1';
 #endif
+    const char* ov = getenv("FMM_OVERLAP_NEAR");
+    P->overlap_near = dim == 3 && P->world == 1 && !collective && ov && ov[0] == '1';
+    if (P->overlap_near) {
+      int lo = 0, hi = 0;
+      FMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // (lo: least, hi: greatest priority)
+      FMM_CUDA(cudaStreamCreateWithPriority(&P->stream2, cudaStreamNonBlocking, hi));
+      FMM_CUDA(cudaStreamCreateWithPriority(&P->stream3, cudaStreamNonBlocking, lo));
+      for (cudaEvent_t* e : {&P->ev_q, &P->ev_up, &P->ev_p2p, &P->ev_far})
+        FMM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
     if (dim == 3) {  // 3D translation operators (the 2D kernels are matrix-free)
       if (P->m2l_variant == 4)
         fmm::m2l_v4_setup(*P);
@@ -382,7 +448,7 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
     cudaEventDestroy(e3);
   });
   if (st != FMM_OK) {
-    delete P;
+    if (P) release_plan(P);
     return st;
   }
   *out = P;
@@ -758,11 +824,7 @@ void fmm_destroy(fmm_plan P) {
   cudaStreamSynchronize(P->stream);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
-  try {
-    fmm::comm_destroy(*P);
-  } catch (...) {
-  }
-  delete P;
+  release_plan(P);
 }
 
 const char* fmm_last_error(void) { return g_last_error.c_str(); }

@@ -83,6 +83,7 @@ struct NearArgs {
   double* grad_out;
   int max_tpl, max_g;  // layout limits (tuning; defaults max_tpl<kGrad>(), 8)
   int64_t out_base;    // perm == nullptr: results at (sorted position - out_base) (LET, owned order)
+  bool p2p_only;       // write the P2P sums (sorted order, unscaled) and skip L2P (overlapped near field)
 };
 
 // Targets [t0, t0 + cnt) of `leaf` as (32 / G) groups x TPL targets per lane.
@@ -198,6 +199,15 @@ __device__ void process_group(const NearArgs& a, int leaf, int t0, int cnt, int 
       }
     const int t = tl + ngrp * kk;
     if (kk < TPL && t < cnt) {
+      if (a.p2p_only) {  // P2P sums only (sorted order, unscaled): L2P later, in l2p_out_kernel
+        a.phi_out[t0 + t] = ff;
+        if (kGrad) {
+          a.grad_out[3 * (t0 + t)] = gg.x;
+          a.grad_out[3 * (t0 + t) + 1] = gg.y;
+          a.grad_out[3 * (t0 + t) + 2] = gg.z;
+        }
+        continue;
+      }
       l2p_eval<kGrad>(Lc, a.p, x.x - c.x, x.y - c.y, x.z - c.z, ff, gg);
       const int64_t o = a.perm ? (int64_t)a.perm[t0 + t] : (int64_t)(t0 + t) - a.out_base;
       a.phi_out[o] = ff * a.s_phi;
@@ -331,10 +341,12 @@ void near_fused_finish(fmm_plan_s& P, double* phi, double* grad) {
   FMM_LAUNCHED("l2p_out_kernel");
 }
 
-void near_pass_warp(fmm_plan_s& P, double* phi, double* grad) {
+namespace {
+void near_launch(fmm_plan_s& P, double* phi, double* grad, bool p2p_only, cudaStream_t stream) {
   const int64_t nl = P.own_leaf_end - P.own_leaf_begin;
   if (nl <= 0) return;
   NearArgs a;
+  a.p2p_only = p2p_only;
   a.cbeg = P.cells.begin;
   a.cend = P.cells.end;
   a.center = P.cells.center;
@@ -344,6 +356,10 @@ void near_pass_warp(fmm_plan_s& P, double* phi, double* grad) {
   a.src = P.p2p.src;
   a.perm = P.near_compact_out ? nullptr : P.perm.ptr;
   a.out_base = P.own_begin;
+  if (p2p_only) {  // sorted order, unscaled
+    a.perm = nullptr;
+    a.out_base = 0;
+  }
   a.p = P.p;
   a.nc = P.nc;
   a.s_phi = std::ldexp(1.0, -P.e);
@@ -361,10 +377,38 @@ void near_pass_warp(fmm_plan_s& P, double* phi, double* grad) {
   const int32_t* leaves = P.leaves.ptr + P.own_leaf_begin;
   const unsigned grid = cdiv(nl, kWarps);
   if (grad)
-    near_warp_kernel<true><<<grid, 32 * kWarps, 0, P.stream>>>(leaves, nl, a);
+    near_warp_kernel<true><<<grid, 32 * kWarps, 0, stream>>>(leaves, nl, a);
   else
-    near_warp_kernel<false><<<grid, 32 * kWarps, 0, P.stream>>>(leaves, nl, a);
+    near_warp_kernel<false><<<grid, 32 * kWarps, 0, stream>>>(leaves, nl, a);
   FMM_LAUNCHED("near_warp_kernel");
+}
+}  // namespace
+
+void near_pass_warp(fmm_plan_s& P, double* phi, double* grad) { near_launch(P, phi, grad, false, P.stream); }
+
+// overlapped near field: the P2P sums on a second stream while the far field
+// (upward, M2L, L2L) runs, then L2P + rescale + scatter to caller order once L is complete
+void near_p2p_async(fmm_plan_s& P, bool grad, cudaStream_t stream) {
+  if (P.near_p2p_phi.count < P.n) P.near_p2p_phi.alloc(P.n);
+  if (grad && P.near_p2p_grad.count < 3 * P.n) P.near_p2p_grad.alloc(3 * P.n);
+  near_launch(P, P.near_p2p_phi, grad ? P.near_p2p_grad.ptr : nullptr, true, stream);
+}
+
+void near_l2p_out(fmm_plan_s& P, double* phi, double* grad) {
+  const int64_t nl = P.own_leaf_end - P.own_leaf_begin;
+  if (nl <= 0) return;
+  const int32_t* leaves = P.leaves.ptr + P.own_leaf_begin;
+  const uint32_t* perm = P.near_compact_out ? nullptr : P.perm.ptr;
+  const double s_phi = std::ldexp(1.0, -P.e), s_grad = std::ldexp(1.0, -2 * P.e);
+  if (grad)
+    l2p_out_kernel<true><<<cdiv(nl, 4), 128, 0, P.stream>>>(leaves, nl, P.cells.begin, P.cells.end, P.cells.center,
+                                                            P.pos, P.L, P.p, P.nc, P.near_p2p_phi, P.near_p2p_grad,
+                                                            perm, P.own_begin, s_phi, s_grad, phi, grad);
+  else
+    l2p_out_kernel<false><<<cdiv(nl, 4), 128, 0, P.stream>>>(leaves, nl, P.cells.begin, P.cells.end,
+                                                             P.cells.center, P.pos, P.L, P.p, P.nc, P.near_p2p_phi,
+                                                             nullptr, perm, P.own_begin, s_phi, s_grad, phi, nullptr);
+  FMM_LAUNCHED("l2p_out_kernel");
 }
 
 }  // namespace fmm

@@ -227,6 +227,10 @@ struct fmm_plan_s {
   fmm::DevBuf<double> near_p2p_phi, near_p2p_grad;  // P2P results in sorted order (unscaled)
   fmm::DevBuf<int> near_counter;                    // next own leaf to take
   bool near_fused_active = false, near_fused_grad = false;  // set for the current mat-vec
+  // near field overlapped with the far field (P2P on a second stream, L2P after L2L)
+  bool overlap_near = false;
+  cudaStream_t stream2 = nullptr, stream3 = nullptr;  // far field (high priority), P2P (low)
+  cudaEvent_t ev_q = nullptr, ev_up = nullptr, ev_p2p = nullptr, ev_far = nullptr;
 
   double t_setup[8] = {0};
   double t_matvec[8] = {0};
@@ -264,6 +268,8 @@ void downward(fmm_plan_s& P);
 void shift_setup(fmm_plan_s& P);  // M2M / L2L term tables
 void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
 void near_pass_warp(fmm_plan_s& P, double* phi, double* grad);
+void near_p2p_async(fmm_plan_s& P, bool grad, cudaStream_t stream);
+void near_l2p_out(fmm_plan_s& P, double* phi, double* grad);
 void near_fused_prepare(fmm_plan_s& P, bool grad);
 void near_fused_finish(fmm_plan_s& P, double* phi, double* grad);
 void gather_charges(fmm_plan_s& P, const double* q);

@@ -395,3 +395,18 @@ def test_m2l_v4_units(torch_cuda, monkeypatch, chunks, dist, n, p, ncrit, theta)
         assert O.rel_l2(phi, phi0) <= 1e-14 and O.rel_l2(g, g0) <= 1e-14
     po, go = O.fmm(x, q, p, ncrit, theta, grad=True, nthreads=O.default_threads())
     assert O.rel_l2(phi, po) <= TOL and O.rel_l2(g, go) <= TOL
+
+
+@pytest.mark.parametrize("dist,n,p,ncrit,theta,grad", [("cube", 20000, 10, 64, 0.4, True),
+                                                       ("plummer", 20000, 6, 32, 0.5, False)])
+def test_overlapped_near_field(torch_cuda, monkeypatch, dist, n, p, ncrit, theta, grad):
+    """FMM_OVERLAP_NEAR=1: the P2P sums on a low-priority stream beside the far field, L2P after
+    L2L (measured not faster, profiles/r2_overlap.md) — results equal the serial path's."""
+    torch = torch_cuda
+    x, q = F.make(dist, n)
+    _, phi0, g0 = gpu_fmm(torch, x, q, p, ncrit, theta, grad=grad)
+    monkeypatch.setenv("FMM_OVERLAP_NEAR", "1")
+    _, phi, g = gpu_fmm(torch, x, q, p, ncrit, theta, grad=grad)
+    assert O.rel_l2(phi, phi0) <= 1e-15
+    if grad:
+        assert O.rel_l2(g, g0) <= 1e-15

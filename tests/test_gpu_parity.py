@@ -410,3 +410,23 @@ def test_overlapped_near_field(torch_cuda, monkeypatch, dist, n, p, ncrit, theta
     assert O.rel_l2(phi, phi0) <= 1e-15
     if grad:
         assert O.rel_l2(g, g0) <= 1e-15
+
+
+def test_repeated_matvecs_bitwise_equal(torch_cuda, monkeypatch):
+    """Stand-in for compute-sanitizer racecheck (closed on this pool, profiles/r2_sanitizer.md):
+    a shared-memory race in the warp-cooperative kernels (M2L v4's copy / in-place stages /
+    segmented sums, the near field's staging) would show up as run-to-run differences; 12
+    repeated mat-vecs, with several M2L v4 unit sizes and warp counts, are bitwise identical."""
+    torch = torch_cuda
+    from paper_1602_02244_b200 import Plan
+
+    x, q = F.make("plummer", 30000)
+    xd, qd = to_dev(torch, x), to_dev(torch, q)
+    for uc, wp in (("0", "0"), ("1", "2"), ("3", "5")):
+        monkeypatch.setenv("FMM_V4_UNIT_CHUNKS", uc)
+        monkeypatch.setenv("FMM_V4_WARPS", wp)
+        pl = Plan(xd, 8, 32, 0.5)
+        ref = pl.matvec(qd, grad=True)
+        for _ in range(12):
+            out = pl.matvec(qd, grad=True)
+            assert torch.equal(out[0], ref[0]) and torch.equal(out[1], ref[1])

@@ -12,10 +12,13 @@ namespace near {
 #endif
 constexpr int kUnroll = FMM_NEAR_UNROLL;
 
-// 1/sqrt(x): rsqrt.approx.f64 seed (MUFU) + one third-order correction y (1 + e/2 + 3e^2/8),
-// e = 1 - x y^2, relative error O(e^3) << 2^-53 (R11)
+// 1/sqrt(x): rsqrt.approx.f64 seed (MUFU, relative error <= 2^-20) refined by one Newton step
+// y (1 + e/2), e = 1 - x y^2: relative error <= 1.5 * 2^-40 = 1.4e-12 per interaction (DESIGN.md
+// R11; measured end-to-end rel-L2 vs the oracle <= 1.4e-13 at every BASELINE config, near field
+// 8 % faster, profiles/r2_near_order.md). FMM_NEAR_ORDER=3: a third-order step y (1 + e/2 +
+// 3e^2/8), relative error O(e^3) << 2^-53.
 #ifndef FMM_NEAR_ORDER
-#define FMM_NEAR_ORDER 3
+#define FMM_NEAR_ORDER 2
 #endif
 __device__ __forceinline__ double rsqrt_fp64(double x) {
   double y;

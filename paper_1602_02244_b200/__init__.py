@@ -4,4 +4,4 @@
 the C ABI of ``include/fmm.h`` (libfmm.so, hand-written CUDA for sm_100a).
 """
 from ._native import FmmError, LIB_PATH  # noqa: F401
-from .fmm import Plan, Plan2D, direct, version  # noqa: F401
+from .fmm import HelmholtzPlan, Plan, Plan2D, direct, direct_helmholtz, version  # noqa: F401

@@ -23,7 +23,8 @@ EXPORTED = ("fmm_setup", "fmm_setup_2d", "fmm_matvec", "fmm_matvec_host", "fmm_s
             "fmm_set_timing", "fmm_export", "fmm_destroy", "fmm_last_error", "fmm_version", "fmm_let_setup",
             "fmm_let_counts", "fmm_let_pack_q", "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack",
             "fmm_let_lists_host", "fmm_stencil_apply", "fmm_precond_setup", "fmm_precond_apply", "fmm_precond_info",
-            "fmm_precond_destroy", "fmm_pcg_solve", "fmm_nccl_unique_id")
+            "fmm_precond_destroy", "fmm_pcg_solve", "fmm_nccl_unique_id", "fmm_setup_helmholtz",
+            "fmm_matvec_helmholtz", "fmm_direct_helmholtz")
 
 
 class FmmExec(C.Structure):
@@ -70,6 +71,10 @@ def lib() -> C.CDLL:
         raise ImportError(f"{LIB_PATH} lacks {missing}: rebuild it (python -m paper_1602_02244_b200.build)")
     vp, dp, i64 = C.c_void_p, C.c_void_p, C.c_int64
     L.fmm_nccl_unique_id.argtypes = [vp]
+    L.fmm_setup_helmholtz.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.c_double,
+                                      C.POINTER(FmmExec)]
+    L.fmm_matvec_helmholtz.argtypes = [vp, dp, i64, dp]
+    L.fmm_direct_helmholtz.argtypes = [dp, dp, i64, dp, i64, C.c_double, dp, C.POINTER(FmmExec)]
     L.fmm_setup.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.POINTER(FmmExec)]
     L.fmm_setup_2d.argtypes = [C.POINTER(C.c_void_p), dp, i64, C.c_int, C.c_int, C.c_double, C.POINTER(FmmExec)]
     L.fmm_matvec.argtypes = [vp, dp, i64, dp, dp]
@@ -104,6 +109,7 @@ def lib() -> C.CDLL:
     for nm in ("fmm_setup", "fmm_setup_2d", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
                "fmm_set_timing", "fmm_export", "fmm_let_setup", "fmm_let_counts", "fmm_let_pack_q",
                "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack", "fmm_let_lists_host", "fmm_nccl_unique_id",
+               "fmm_setup_helmholtz", "fmm_matvec_helmholtz", "fmm_direct_helmholtz",
                "fmm_stencil_apply",
                "fmm_precond_setup", "fmm_precond_apply", "fmm_precond_info", "fmm_pcg_solve"):
         getattr(L, nm).restype = C.c_int

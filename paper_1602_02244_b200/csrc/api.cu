@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 
+#include "../../include/fmm_helmholtz.h"
 #include "plan.h"
 
 namespace {
@@ -314,7 +315,7 @@ int64_t fmm_plan_s::bytes() const {
        cells.parent.bytes() + cells.anchor.bytes() + cells.center.bytes();
   b += p2p.tgt.bytes() + p2p.src.bytes() + p2p.off.bytes() + m2l.tgt.bytes() + m2l.src.bytes() + m2l.off.bytes();
   b += host_stage_q.bytes() + host_stage_phi.bytes() + host_stage_grad.bytes();
-  b += m2l_dmma.bytes() + m2l4.bytes();
+  b += m2l_dmma.bytes() + m2l4.bytes() + helm.bytes();
   b += shift_ops.bytes();
   b += let_dev.bytes();
   return b;
@@ -339,7 +340,7 @@ void release_plan(fmm_plan_s* P) {
 }
 
 fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int ncrit, double theta,
-                      const fmm_exec* ex, int dim) {
+                      const fmm_exec* ex, int dim, double kappa = 0.0) {
   if (!out) return fail(FMM_ERR_USAGE, "fmm_setup: out is NULL");
   *out = nullptr;
   fmm_plan_s* P = nullptr;
@@ -415,7 +416,13 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
       for (cudaEvent_t* e : {&P->ev_q, &P->ev_up, &P->ev_p2p, &P->ev_far})
         FMM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    if (dim == 3) {  // 3D translation operators (the 2D kernels are matrix-free)
+    if (kappa > 0.0) {  // Helmholtz (NEXT-4): its own level / class tables (helmholtz.cu)
+      usage(P->world == 1 && !collective, "fmm_setup_helmholtz: single GPU only");
+      P->helmholtz = true;
+      P->kappa = kappa;
+      P->m2l_variant = 5;
+      fmm::helmholtz_setup(*P);
+    } else if (dim == 3) {  // 3D translation operators (the 2D kernels are matrix-free)
       if (P->m2l_variant == 4)
         fmm::m2l_v4_setup(*P);
       else if (P->m2l_variant >= 2)
@@ -479,10 +486,53 @@ fmm_status fmm_setup_2d(fmm_plan* out, const double* xy, int64_t n, int p, int n
   return setup_impl(out, xyz, n, p, ncrit, theta, ex, 2);
 }
 
+fmm_status fmm_setup_helmholtz(fmm_plan* out, const double* xyz, int64_t n, int p, int ncrit, double theta,
+                               double kappa, const fmm_exec* ex) {
+  if (!out) return fail(FMM_ERR_USAGE, "fmm_setup_helmholtz: out is NULL");
+  *out = nullptr;
+  if (!(kappa > 0.0) || !std::isfinite(kappa)) return fail(FMM_ERR_USAGE, "fmm_setup_helmholtz: kappa must be > 0");
+  if (p < 0 || p > 10) return fail(FMM_ERR_USAGE, "fmm_setup_helmholtz: p must be in [0, 10]");
+  if (ex && (ex->world_size != 1 || ex->nccl_id)) return fail(FMM_ERR_USAGE, "fmm_setup_helmholtz: single GPU only");
+  return setup_impl(out, xyz, n, p, ncrit, theta, ex, 3, kappa);
+}
+
+fmm_status fmm_matvec_helmholtz(fmm_plan P, const double* q, int64_t n, double* phi) {
+  if (!P) return fail(FMM_ERR_USAGE, "fmm_matvec_helmholtz: plan is NULL");
+  if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_matvec_helmholtz: plan is poisoned by an earlier error");
+  return guarded(P, [&] {
+    usage(P->helmholtz, "fmm_matvec_helmholtz: not a Helmholtz plan (fmm_setup_helmholtz)");
+    usage(n == P->n, "fmm_matvec_helmholtz: n differs from the setup n");
+    usage(q != nullptr && phi != nullptr, "fmm_matvec_helmholtz: q / phi is NULL");
+    FMM_CUDA(cudaSetDevice(P->device));
+    Timer T(*P, P->timing);
+    T.mark(0);
+    fmm::helmholtz_matvec(*P, q, phi);
+    T.mark(4);
+    if (T.on) {
+      FMM_CUDA(cudaEventSynchronize(P->ev[4]));
+      P->t_matvec[FMM_T_MATVEC_TOTAL] = T.between(0, 4);
+    }
+  });
+}
+
+fmm_status fmm_direct_helmholtz(const double* src, const double* q, int64_t ns, const double* tgt, int64_t nt,
+                                double kappa, double* phi, const fmm_exec* ex) {
+  return guarded(nullptr, [&] {
+    usage(ex != nullptr, "fmm_direct_helmholtz: ex is NULL");
+    usage(ns >= 0 && nt >= 0, "fmm_direct_helmholtz: negative size");
+    usage(ns == 0 || (src && q), "fmm_direct_helmholtz: src / q is NULL");
+    usage(nt == 0 || (tgt && phi), "fmm_direct_helmholtz: tgt / phi is NULL");
+    usage(std::isfinite(kappa), "fmm_direct_helmholtz: kappa must be finite");
+    FMM_CUDA(cudaSetDevice(ex->device));
+    fmm::helmholtz_direct(src, q, ns, tgt, nt, kappa, phi, (cudaStream_t)ex->stream);
+  });
+}
+
 fmm_status fmm_matvec(fmm_plan P, const double* q, int64_t n, double* phi, double* grad) {
   if (!P) return fail(FMM_ERR_USAGE, "fmm_matvec: plan is NULL");
   if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_matvec: plan is poisoned by an earlier error");
   return guarded(P, [&] {
+    usage(!P->helmholtz, "fmm_matvec: a Helmholtz plan takes fmm_matvec_helmholtz");
     if (P->collective) {  // this rank's caller slice in and out; collective over the world
       usage(n == P->n_local, "fmm_matvec: n differs from this rank's setup slice");
       usage(n == 0 || (q != nullptr && phi != nullptr), "fmm_matvec: q / phi is NULL");
@@ -501,6 +551,7 @@ fmm_status fmm_matvec_host(fmm_plan P, const double* q_host, int64_t n, double* 
   if (!P) return fail(FMM_ERR_USAGE, "fmm_matvec_host: plan is NULL");
   if (P->poisoned) return fail(FMM_ERR_USAGE, "fmm_matvec_host: plan is poisoned by an earlier error");
   return guarded(P, [&] {
+    usage(!P->helmholtz, "fmm_matvec_host: a Helmholtz plan takes fmm_matvec_helmholtz");
     const int64_t nn = P->collective ? P->n_local : P->n;
     usage(n == nn, "fmm_matvec_host: n differs from the setup n (collective mode: this rank's slice)");
     usage(n == 0 || (q_host != nullptr && phi_host != nullptr), "fmm_matvec_host: q / phi is NULL");
@@ -573,19 +624,21 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     const fmm::Cells& c = P->cells;
     int64_t* b = out->bytes_by;
     for (int k = 0; k < 8; ++k) b[k] = 0;
-    b[FMM_B_PARTICLES] = P->keys.bytes() + P->perm.bytes() + P->pos.bytes() + P->host_stage_q.bytes() +
+    b[FMM_B_PARTICLES] = P->keys.bytes() + P->perm.bytes() + P->pos.bytes() + P->helm.qs.bytes() + P->host_stage_q.bytes() +
                          P->host_stage_phi.bytes() + P->host_stage_grad.bytes();
     b[FMM_B_TREE] = c.level.bytes() + c.begin.bytes() + c.end.bytes() + c.child.bytes() + c.nchild.bytes() +
                     c.parent.bytes() + c.anchor.bytes() + c.center.bytes() + P->leaves.bytes() + P->m2l4.ihalf.bytes();
     b[FMM_B_LISTS] = P->p2p.tgt.bytes() + P->p2p.src.bytes() + P->p2p.off.bytes() + P->m2l.tgt.bytes() +
                      P->m2l.src.bytes() + P->m2l.off.bytes();
-    b[FMM_B_EXPANSIONS] = P->M.bytes() + P->L.bytes() + D.Mt.bytes() + P->m2l4.Mt.bytes();
+    b[FMM_B_EXPANSIONS] = P->M.bytes() + P->L.bytes() + D.Mt.bytes() + P->m2l4.Mt.bytes() + P->helm.M.bytes() +
+                          P->helm.L.bytes();
     b[FMM_B_OPERATORS] = D.ops.bytes() + D.rot_ops.bytes() + D.hpow.bytes() + D.symtab.bytes() +
-                         D.rot_masks.bytes() + D.class_keys.bytes() + P->shift_ops.bytes();
+                         D.rot_masks.bytes() + D.class_keys.bytes() + P->shift_ops.bytes() + P->helm.shift_ops.bytes() +
+                         P->helm.m2l_ops.bytes();
     b[FMM_B_SCHEDULE] = D.col_src.bytes() + D.col_meta.bytes() + D.chunk_begin.bytes() + D.chunk_class.bytes() +
                         D.tile_chunk.bytes() + D.tile_cells.bytes() + D.chunk_seg.bytes() + D.seg_begin.bytes() +
                         D.rot_sched.bytes() + D.rot_ihdr.bytes() + D.rot_ipos.bytes() + D.rot_desc.bytes() +
-                        D.rot_order.bytes() + D.rot_scratch.bytes() + P->m2l4.part.bytes();
+                        D.rot_order.bytes() + D.rot_scratch.bytes() + P->m2l4.part.bytes() + P->helm.m2l_class.bytes();
     b[FMM_B_LET] = P->let_dev.bytes();
     int64_t s = 0;
     for (int k = 0; k < 7; ++k) s += b[k];
@@ -594,7 +647,9 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
   out->m2l_variant = P->m2l_variant;
   {
     const double p1 = P->p + 1;
-    if (P->dim == 2) {  // 2D log kernel: one complex multiply-add per (l, k) pair
+    if (P->helmholtz) {  // dense complex (S|R) class operator: 8 flop per complex MAC
+      out->m2l_flops_per_pair = 8.0 * p1 * p1 * p1 * p1;
+    } else if (P->dim == 2) {  // 2D log kernel: one complex multiply-add per (l, k) pair
       out->m2l_variant = 0;
       out->m2l_flops_per_pair = 8.0 * p1 * p1;
     } else if (P->m2l_variant == 4) {  // per degree 2 (n^2+n+1) fixed-operator MACs + 2 zrot (4 n), twice;

@@ -117,6 +117,19 @@ struct M2L4 {
   int64_t bytes() const { return Mt.bytes() + part.bytes() + ihalf.bytes(); }
 };
 
+// Helmholtz plan state (helmholtz.cu, NEXT-4)
+struct HelmState {
+  DevBuf<double2> qs;         // [n] charges in Morton order
+  DevBuf<double2> M, L;       // [ncells][(p+1)^2] spherical-wave expansions
+  DevBuf<double2> shift_ops;  // [levels][8][2][(p+1)^2]^2 (S|S) for M2M, (R|R) for L2L, transposed
+  DevBuf<double2> m2l_ops;    // [nclass][(p+1)^2]^2 (S|R), transposed
+  DevBuf<int32_t> m2l_class;  // [npairs] class of every M2L pair
+  int64_t nclass = 0;
+  int64_t bytes() const {
+    return qs.bytes() + M.bytes() + L.bytes() + shift_ops.bytes() + m2l_ops.bytes() + m2l_class.bytes();
+  }
+};
+
 // LET exchange lists of one rank (let.cu); counts per peer rank, index lists concatenated in rank order.
 struct LetLists {
   int world = 1;
@@ -160,6 +173,9 @@ struct fmm_plan_s {
   cudaStream_t stream = nullptr;
   int rank = 0, world = 1;
   int dim = 3;  // 2: planar points (x, y, 0) with the 2D log kernel (fmm2d.cu, fmm_setup_2d)
+  bool helmholtz = false;  // exp(i kappa r) / r kernel (helmholtz.cu, fmm_setup_helmholtz)
+  double kappa = 0;
+  fmm::HelmState helm;
   bool poisoned = false;
   bool timing = false;
   bool debug_skip_l2l = false;
@@ -268,6 +284,10 @@ void downward(fmm_plan_s& P);
 void shift_setup(fmm_plan_s& P);  // M2M / L2L term tables
 void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
 void near_pass_warp(fmm_plan_s& P, double* phi, double* grad);
+void helmholtz_setup(fmm_plan_s& P);
+void helmholtz_matvec(fmm_plan_s& P, const double* q, double* phi);
+void helmholtz_direct(const double* src, const double* q, int64_t ns, const double* tgt, int64_t nt, double kappa,
+                      double* phi, cudaStream_t s);
 void near_p2p_async(fmm_plan_s& P, bool grad, cudaStream_t stream);
 void near_l2p_out(fmm_plan_s& P, double* phi, double* grad);
 void near_fused_prepare(fmm_plan_s& P, bool grad);

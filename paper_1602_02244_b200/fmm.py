@@ -189,6 +189,54 @@ class Plan2D(Plan):
     _dim = 2
 
 
+def _dev_c128(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.complex128 or t.dim() != 1:
+        raise TypeError(f"{name} must be a 1-D CUDA complex128 tensor")
+    return t.contiguous()
+
+
+class HelmholtzPlan(Plan):
+    """NEXT-4: FMM plan for the 3D Helmholtz kernel exp(i kappa r) / r
+    (``fmm_setup_helmholtz``, include/fmm_helmholtz.h); ``matvec`` maps complex128 charges to
+    complex128 potentials, caller order. Single GPU."""
+
+    def __init__(self, points: torch.Tensor, p: int, ncrit: int, theta: float, kappa: float, *, stream=None):
+        points = _dev_f64(points, "points", (3,))
+        self.device = points.device
+        self.n = points.shape[0]
+        self.p, self.ncrit, self.theta, self.kappa = p, ncrit, theta, float(kappa)
+        self.rank, self.world = 0, 1
+        self._stream = stream
+        self._nccl_id = None
+        self._ex = _exec(self.device, stream, 0, 1)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            N.check(N.lib().fmm_setup_helmholtz(C.byref(h), C.c_void_p(points.data_ptr()), self.n, p, ncrit,
+                                                float(theta), float(kappa), C.byref(self._ex)))
+        self._h = h
+
+    def matvec(self, q: torch.Tensor, out: torch.Tensor | None = None):
+        q = _dev_c128(q, "q")
+        if q.shape[0] != self.n:
+            raise ValueError("q length differs from the plan's point count")
+        phi = torch.empty(self.n, dtype=torch.complex128, device=self.device) if out is None else out
+        N.check(N.lib().fmm_matvec_helmholtz(self._h, C.c_void_p(q.data_ptr()), self.n, C.c_void_p(phi.data_ptr())))
+        return phi
+
+
+def direct_helmholtz(src: torch.Tensor, q: torch.Tensor, kappa: float, tgt: torch.Tensor | None = None):
+    """fmm_direct_helmholtz: O(n_src n_tgt) sum of q exp(i kappa r) / r on the GPU (checking path)."""
+    src = _dev_f64(src, "src", (3,))
+    q = _dev_c128(q, "q")
+    tgt = src if tgt is None else _dev_f64(tgt, "tgt", (3,))
+    phi = torch.empty(tgt.shape[0], dtype=torch.complex128, device=src.device)
+    ex = _exec(src.device)
+    N.check(N.lib().fmm_direct_helmholtz(C.c_void_p(src.data_ptr()), C.c_void_p(q.data_ptr()), src.shape[0],
+                                         C.c_void_p(tgt.data_ptr()), tgt.shape[0], float(kappa),
+                                         C.c_void_p(phi.data_ptr()), C.byref(ex)))
+    return phi
+
+
 def direct(src: torch.Tensor, q: torch.Tensor, tgt: torch.Tensor | None = None, grad: bool = False):
     """fmm_direct: O(n_src n_tgt) sum on the GPU (checking path, north_star)."""
     src = _dev_f64(src, "src", (3,))

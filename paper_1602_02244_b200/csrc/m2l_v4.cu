@@ -371,26 +371,34 @@ __device__ __forceinline__ void stage3(double* w, const double2* ca, const doubl
 // (the empty asm with a memory clobber keeps the compiler from hoisting the next degree's
 // shared-memory loads above this degree's stores: one degree / order live at a time)
 __device__ __forceinline__ void order_fence() { asm volatile("" ::: "memory"); }
+// blocks smaller than this many degrees are not fenced (the compiler may overlap them: more ILP
+// where one degree / order alone has little)
+#ifndef FMM_V4_STAGE_SYNC
+#define FMM_V4_STAGE_SYNC 1  // CTA barriers after stages 1 and 2 too (else once per chunk)
+#endif
+#ifndef FMM_V4_FENCE_MIN
+#define FMM_V4_FENCE_MIN 0
+#endif
 
 template <int P, int N = 0>
 __device__ __forceinline__ void stage1_all(double* w, double r, double rn, const double2* ca, const double2* cb,
                                            const int (&z)[4]) {
   stage1<N>(w, rn, ca, cb, z[0], z[1]);
-  order_fence();
+  if constexpr (N >= FMM_V4_FENCE_MIN) order_fence();
   if constexpr (N < P) stage1_all<P, N + 1>(w, r, rn * r, ca, cb, z);
 }
 template <int P, int M = 0>
 __device__ __forceinline__ void stage2_all(double* w, const double* h) {
   stage2<P, M, 0>(w, h);
-  order_fence();
+  if constexpr (P - M >= FMM_V4_FENCE_MIN) order_fence();
   if constexpr (M > 0) stage2<P, M, 1>(w, h);
-  order_fence();
+  if constexpr (P - M >= FMM_V4_FENCE_MIN) order_fence();
   if constexpr (M < P) stage2_all<P, M + 1>(w, h);
 }
 template <int P, int N = 0>
 __device__ __forceinline__ void stage3_all(double* w, const double2* ca, const double2* cb, const int (&z)[4]) {
   stage3<N>(w, ca, cb, z[2], z[3]);
-  order_fence();
+  if constexpr (N >= FMM_V4_FENCE_MIN) order_fence();
   if constexpr (N < P) stage3_all<P, N + 1>(w, ca, cb, z);
 }
 
@@ -504,7 +512,7 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
         sr_next = nb < u1 ? a.src[nb] : 0;
       }
       // 1. source rows into the lanes' buffers (coalesced: row by row)
-#pragma unroll 4
+#pragma unroll 8
       for (int l = 0; l < nact; ++l) {
         const int s = __shfl_sync(0xffffffffu, sr, l);
         const double* g = a.Mt + (int64_t)s * NR;
@@ -557,29 +565,54 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
 #pragma unroll
         for (int k = 0; k < 4; ++k) z[k] = (zc * (k + 1)) & a.zmask;
         stage1_all<P>(w, r, 1.0, ca, cb, z);
+#if FMM_V4_STAGE_SYNC
         __syncthreads();
+#endif
         double h[2 * P + 1];  // Hankel entries k! / u^{k+1}
         h[0] = iu;
 #pragma unroll
         for (int k = 1; k <= 2 * P; ++k) h[k] = h[k - 1] * (k * iu);
         stage2_all<P>(w, h);
+#if FMM_V4_STAGE_SYNC
         __syncthreads();
+#endif
         stage3_all<P>(w, ca, cb, z);
       }
       __syncwarp();
-      // 3. segmented sum over lanes with the same target (lane order)
-      for (int l = 0; l < nact; ++l) {
-        const int t = __shfl_sync(0xffffffffu, tg, l);
-        if (t != cur) {
-          if (cur >= 0) finish_segment<P>(a, u, cur, cur == tprev, false, acc, lane);
-          cur = t;
+      // 3. segmented sum over lanes with the same target: segments (runs of one target in the
+      // target-grouped list) from a ballot; within a segment four interleaved partial sums
+      // (rows s0+k, s0+k+4, ...) combined as (p0 + p1) + (p2 + p3): a fixed order, four
+      // independent add chains per coefficient instead of one
+      {
+        const int prev_tg = __shfl_up_sync(0xffffffffu, tg, 1);
+        unsigned starts = __ballot_sync(0xffffffffu, act && (lane == 0 || tg != prev_tg));
+        while (starts) {
+          const int s0 = __ffs(starts) - 1;
+          starts &= starts - 1;
+          const int s1 = starts ? __ffs(starts) - 1 : nact;
+          const int t = __shfl_sync(0xffffffffu, tg, s0);
+          if (t != cur) {
+            if (cur >= 0) finish_segment<P>(a, u, cur, cur == tprev, false, acc, lane);
+            cur = t;
 #pragma unroll
-          for (int c = 0; c < KPL; ++c) acc[c] = 0.0;
+            for (int c = 0; c < KPL; ++c) acc[c] = 0.0;
+          }
+#pragma unroll
+          for (int c = 0; c < KPL; ++c) {
+            const int k = lane + 32 * c;
+            if (k >= NR) continue;
+            double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+            int l = s0;
+            for (; l + 3 < s1; l += 4) {
+              p0 += wb[l * NRS + k];
+              p1 += wb[(l + 1) * NRS + k];
+              p2 += wb[(l + 2) * NRS + k];
+              p3 += wb[(l + 3) * NRS + k];
+            }
+            for (; l < s1; ++l) p0 += wb[l * NRS + k];
+            acc[c] += (p0 + p1) + (p2 + p3);
+          }
         }
-        const double* row = wb + l * NRS;
-#pragma unroll
-        for (int c = 0; c < KPL; ++c)
-          if (lane + 32 * c < NR) acc[c] += row[lane + 32 * c];
       }
       __syncthreads();
     }

@@ -23,8 +23,13 @@ constexpr int kUnroll = FMM_NEAR_UNROLL;
 __device__ __forceinline__ double rsqrt_fp64(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  if (FMM_NEAR_ORDER == 2) {  // one Newton step y + y (1 - x y^2) / 2, the halving of y done on
+    // the exponent (integer pipe; y is a positive normal number): 3 FP64 ops instead of 4,
+    // bitwise the same result (scaling by 2 commutes with rounding)
+    const double yh = __hiloint2double(__double2hiint(y) - 0x00100000, __double2loint(y));
+    return fma(y, fma(-x * yh, y, 0.5), y);
+  }
   const double e = fma(-x * y, y, 1.0);  // 1 - x y^2
-  if (FMM_NEAR_ORDER == 2) return fma(y, 0.5 * e, y);  // one Newton step
   const double c = e * fma(e, 0.375, 0.5);  // e/2 + 3 e^2/8
   return fma(y, c, y);
 }

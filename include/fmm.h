@@ -104,7 +104,9 @@ typedef struct {
                             operators on DMMA, 3 rotation-factored class operators on DMMA,
                             4 per-pair rotation on DFMA with one fixed operator (default,
                             2 <= p <= 12); 0 for a 2D (log-kernel) plan (complex series) */
-  int m2l_pad_;
+  int near_mutual;       /* 1: potentials-only mat-vecs evaluate each unordered P2P leaf pair once
+                            (single GPU, symmetric lists, leaves <= 64 particles; FMM_NEAR_MUTUAL=0
+                            disables), 0: directed P2P */
   double m2l_flops_per_pair; /* flops per M2L pair of that formulation as executed (v4: the four
                                 fixed-operator products, four z-rotations and the Hankel
                                 translation; v3: the three block stages + the two azimuthal
@@ -115,9 +117,9 @@ typedef struct {
                                 setup included): differences count a region's launches */
 } fmm_stats_t;
 enum {
-  FMM_B_PARTICLES = 0,  /* keys, permutation, positions + charges, host-call staging */
+  FMM_B_PARTICLES = 0,  /* keys, permutation, positions + charges, host-call staging, mutual near-field sums */
   FMM_B_TREE = 1,       /* cell arrays, leaf index */
-  FMM_B_LISTS = 2,      /* P2P and M2L interaction lists */
+  FMM_B_LISTS = 2,      /* P2P and M2L interaction lists (+ the mutual near field's task lists) */
   FMM_B_EXPANSIONS = 3, /* M and L, plus the M2L kernels' scaled multipole rows */
   FMM_B_OPERATORS = 4,  /* precomputed translation operators: M2L class tables, M2M/L2L */
   FMM_B_SCHEDULE = 5,   /* M2L column / chunk / tile schedules and descriptors */

@@ -39,7 +39,7 @@ class FmmStats(C.Structure):
         ("own_end", C.c_int64), ("p", C.c_int32), ("ncrit", C.c_int32), ("max_level", C.c_int32),
         ("exponent", C.c_int32), ("theta", C.c_double), ("t_setup_ms", C.c_double * 8),
         ("t_matvec_ms", C.c_double * 8), ("bytes_device", C.c_int64), ("m2l_variant", C.c_int32),
-        ("m2l_pad_", C.c_int32), ("m2l_flops_per_pair", C.c_double), ("bytes_by", C.c_int64 * 8), ("launches_total", C.c_int64),
+        ("near_mutual", C.c_int32), ("m2l_flops_per_pair", C.c_double), ("bytes_by", C.c_int64 * 8), ("launches_total", C.c_int64),
     ]
 BYTES_CATEGORIES = ("particles", "tree", "lists", "expansions", "operators", "schedule", "let", "other")
 

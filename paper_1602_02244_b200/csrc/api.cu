@@ -196,6 +196,8 @@ void run_matvec(fmm_plan_s& P, const double* q, double* phi, double* grad) {
   }
   if (P.near_fused_active)
     fmm::near_fused_finish(P, phi, grad);
+  else if (P.near_variant == 2 && P.mutual.enabled && !grad)
+    fmm::near_mutual_pass(P, phi);
   else if (P.near_variant == 2)
     fmm::near_pass_warp(P, phi, grad);
   else
@@ -315,7 +317,7 @@ int64_t fmm_plan_s::bytes() const {
        cells.parent.bytes() + cells.anchor.bytes() + cells.center.bytes();
   b += p2p.tgt.bytes() + p2p.src.bytes() + p2p.off.bytes() + m2l.tgt.bytes() + m2l.src.bytes() + m2l.off.bytes();
   b += host_stage_q.bytes() + host_stage_phi.bytes() + host_stage_grad.bytes();
-  b += m2l_dmma.bytes() + m2l4.bytes() + helm.bytes();
+  b += m2l_dmma.bytes() + m2l4.bytes() + helm.bytes() + mutual.bytes();
   b += shift_ops.bytes();
   b += let_dev.bytes();
   return b;
@@ -428,6 +430,9 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
       else if (P->m2l_variant >= 2)
         fmm::m2l_dmma_setup(*P);
       fmm::shift_setup(*P);
+      const char* mu = getenv("FMM_NEAR_MUTUAL");  // 0: directed P2P for potentials too
+      if (P->near_variant == 2 && !collective && P->world == 1 && !(mu && mu[0] == '0'))
+        fmm::near_mutual_setup(*P);
     }
     P->M.alloc(P->cells.n * P->nc);
     if (collective) {  // exchange lists and buffers of this rank (let.cu)
@@ -625,11 +630,13 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     int64_t* b = out->bytes_by;
     for (int k = 0; k < 8; ++k) b[k] = 0;
     b[FMM_B_PARTICLES] = P->keys.bytes() + P->perm.bytes() + P->pos.bytes() + P->helm.qs.bytes() + P->host_stage_q.bytes() +
-                         P->host_stage_phi.bytes() + P->host_stage_grad.bytes();
+                         P->host_stage_phi.bytes() + P->host_stage_grad.bytes() + P->mutual.partial.bytes() +
+                         P->mutual.own.bytes();
     b[FMM_B_TREE] = c.level.bytes() + c.begin.bytes() + c.end.bytes() + c.child.bytes() + c.nchild.bytes() +
                     c.parent.bytes() + c.anchor.bytes() + c.center.bytes() + P->leaves.bytes() + P->m2l4.ihalf.bytes();
     b[FMM_B_LISTS] = P->p2p.tgt.bytes() + P->p2p.src.bytes() + P->p2p.off.bytes() + P->m2l.tgt.bytes() +
-                     P->m2l.src.bytes() + P->m2l.off.bytes();
+                     P->m2l.src.bytes() + P->m2l.off.bytes() + P->mutual.toff.bytes() + P->mutual.task_b.bytes() +
+                     P->mutual.poff.bytes() + P->mutual.goff.bytes() + P->mutual.gslot.bytes();
     b[FMM_B_EXPANSIONS] = P->M.bytes() + P->L.bytes() + D.Mt.bytes() + P->m2l4.Mt.bytes() + P->helm.M.bytes() +
                           P->helm.L.bytes();
     b[FMM_B_OPERATORS] = D.ops.bytes() + D.rot_ops.bytes() + D.hpow.bytes() + D.symtab.bytes() +
@@ -645,6 +652,7 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     b[FMM_B_OTHER] = out->bytes_device - s;
   }
   out->m2l_variant = P->m2l_variant;
+  out->near_mutual = P->mutual.enabled ? 1 : 0;
   {
     const double p1 = P->p + 1;
     if (P->helmholtz) {  // dense complex (S|R) class operator: 8 flop per complex MAC

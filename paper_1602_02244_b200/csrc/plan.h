@@ -117,6 +117,20 @@ struct M2L4 {
   int64_t bytes() const { return Mt.bytes() + part.bytes() + ihalf.bytes(); }
 };
 
+// mutual near field (near_mutual.cu): each unordered leaf pair evaluated once, single GPU, potentials
+struct NearMutual {
+  bool enabled = false;
+  DevBuf<int32_t> toff, task_b;  // tasks (A, B > A) grouped by A: [ncells + 1], [ntasks]
+  DevBuf<int64_t> poff;          // [ntasks] B-side partial slot
+  DevBuf<int32_t> goff;          // [ncells + 1] per leaf, its B-side slots (gslot) in list order
+  DevBuf<int64_t> gslot;
+  DevBuf<double> partial, own;   // [sum of |B| over tasks], [n] (sorted order)
+  int64_t ntasks = 0;
+  int64_t bytes() const {
+    return toff.bytes() + task_b.bytes() + poff.bytes() + goff.bytes() + gslot.bytes() + partial.bytes() + own.bytes();
+  }
+};
+
 // Helmholtz plan state (helmholtz.cu, NEXT-4)
 struct HelmState {
   DevBuf<double2> qs;         // [n] charges in Morton order
@@ -210,6 +224,7 @@ struct fmm_plan_s {
                         // 4 = per-pair rotation on DFMA with a fixed constant-bank operator
                         //     (2 <= p <= 12; else v3)
   int near_variant = 2; // 1 = block per leaf, thread per target (v1), 2 = warp per leaf (v2)
+  fmm::NearMutual mutual;  // v2 potentials-only, single GPU: symmetric leaf pairs once (FMM_NEAR_MUTUAL)
 
   // this rank's targets (Morton range of sorted positions) and its leaves
   int64_t own_begin = 0, own_end = 0;
@@ -284,6 +299,8 @@ void downward(fmm_plan_s& P);
 void shift_setup(fmm_plan_s& P);  // M2M / L2L term tables
 void near_pass(fmm_plan_s& P, const double* q_unused, double* phi, double* grad);
 void near_pass_warp(fmm_plan_s& P, double* phi, double* grad);
+void near_mutual_setup(fmm_plan_s& P);
+void near_mutual_pass(fmm_plan_s& P, double* phi);
 void helmholtz_setup(fmm_plan_s& P);
 void helmholtz_matvec(fmm_plan_s& P, const double* q, double* phi);
 void helmholtz_direct(const double* src, const double* q, int64_t ns, const double* tgt, int64_t nt, double kappa,

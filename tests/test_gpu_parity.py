@@ -431,3 +431,45 @@ def test_repeated_matvecs_bitwise_equal(torch_cuda, monkeypatch):
         for _ in range(12):
             out = pl.matvec(qd, grad=True)
             assert torch.equal(out[0], ref[0]) and torch.equal(out[1], ref[1])
+
+
+@pytest.mark.parametrize("dist,n,p,ncrit,theta", [("cube", 30000, 10, 64, 0.4), ("plummer", 20000, 6, 32, 0.5),
+                                                  ("sphere", 20000, 8, 16, 0.4), ("plummer", 8000, 3, 7, 0.3),
+                                                  ("cube", 3000, 2, 16, 1e-6), ("cube", 4000, 4, 1, 0.4)])
+def test_mutual_near_field(torch_cuda, monkeypatch, dist, n, p, ncrit, theta):
+    """Potentials-only mat-vecs evaluate each unordered P2P leaf pair once (csrc/near_mutual.cu):
+    oracle parity, agreement with the directed P2P (FMM_NEAR_MUTUAL=0) to rounding, and bitwise
+    repeatability (its sums have a fixed order: per-task partial slots, no atomics)."""
+    torch = torch_cuda
+    from paper_1602_02244_b200 import Plan
+
+    x, q = F.make(dist, n)
+    xd, qd = to_dev(torch, x), to_dev(torch, q)
+    pl = Plan(xd, p, ncrit, theta)
+    assert pl.stats()["near_mutual"] == 1
+    phi = pl.matvec(qd)
+    for _ in range(5):
+        assert torch.equal(pl.matvec(qd), phi)
+    phi = phi.cpu().numpy()
+    ref = O.fmm(x, q, p, ncrit, theta, nthreads=O.default_threads())
+    tol = 2e-12 if theta < 1e-3 else TOL  # all-P2P case: as test_near_variants
+    assert O.rel_l2(phi, ref) <= tol
+    monkeypatch.setenv("FMM_NEAR_MUTUAL", "0")
+    pd = Plan(xd, p, ncrit, theta)
+    assert pd.stats()["near_mutual"] == 0
+    assert O.rel_l2(phi, pd.matvec(qd).cpu().numpy()) <= 1e-14
+    # gradients always take the directed path on the same plan
+    g = pl.matvec(qd, grad=True)
+    gd = pd.matvec(qd, grad=True)
+    assert torch.equal(g[0], gd[0]) and torch.equal(g[1], gd[1])
+
+
+def test_mutual_near_field_limits(torch_cuda):
+    """Leaves above 64 particles keep the directed P2P (the mutual kernel's register layout)."""
+    torch = torch_cuda
+    from paper_1602_02244_b200 import Plan
+
+    x, q = F.make("cube", 8000)  # 8000 / 64 = 125 per level-2 cell: leaves of ~125 particles
+    pl = Plan(to_dev(torch, x), 4, 200, 0.4)
+    assert pl.stats()["near_mutual"] == 0
+    assert pl.matvec(to_dev(torch, q)).shape == (8000,)

@@ -52,6 +52,10 @@
 
 #include "plan.h"
 
+#ifndef FMM_V4_CIMM
+#define FMM_V4_CIMM 1  // pair code as a called function: fixed-operator entries at immediate addresses (LDCU.128)
+#endif
+
 namespace fmm {
 namespace m2l4 {
 
@@ -288,7 +292,14 @@ template <int N, bool T, bool SG, bool SX, int I>
 __device__ __forceinline__ void fstep(const double (&x)[2 * N + 1], double (&y)[2 * N + 1], int z) {
   constexpr FEnt E = FTabOf<N>::value.e[I];
   constexpr bool neg = (SG && E.gneg) != (SX && (T ? sx_neg(E.mrow, E.prow) : sx_neg(E.mcol, E.pcol)));
+#if FMM_V4_CIMM
+  // immediate constant-bank address behind a volatile asm: not hoisted out of the pair loop by
+  // the compiler, folded by ptxas into the DFMA's c[0x3][imm] operand (no load instruction)
+  const double f = fmm_c_F4[offF(N) + I];
+  (void)z;
+#else
   const double f = fmm_c_F4[offF(N) + I + 2 * z];  // (2 z: 16-byte aligned, LDCU.128 pairs)
+#endif
   const double c = neg ? -f : f;
   if constexpr (!T)
     y[E.r] = fma(c, x[E.k], y[E.r]);
@@ -476,6 +487,38 @@ __device__ __forceinline__ void finish_segment(const V4Args& a, int64_t u, int t
     if (lane + 32 * c < NR) d[lane + 32 * c] = acc[c];
 }
 
+#if FMM_V4_CIMM
+// one pair's rotation-translation-rotation, in place in the lane's row w. Not inlined: the fixed
+// operator's constant-bank entries are then DFMA operands at immediate addresses (no load
+// instruction) that the compiler cannot hoist out of the chunk loop into registers.
+template <int P>
+__device__ __noinline__ void pair_transform(double* w, double r, double2 e1, double2 e2, double iu) {
+  double2 ca[P + 1], cb[P + 1];
+  ca[0] = cb[0] = make_double2(1.0, 0.0);
+  ca[1] = e1;
+  cb[1] = e2;
+#pragma unroll
+  for (int m = 2; m <= P; ++m) {
+    ca[m] = make_double2(fma(ca[m - 1].x, e1.x, -ca[m - 1].y * e1.y), fma(ca[m - 1].x, e1.y, ca[m - 1].y * e1.x));
+    cb[m] = make_double2(fma(cb[m - 1].x, e2.x, -cb[m - 1].y * e2.y), fma(cb[m - 1].x, e2.y, cb[m - 1].y * e2.x));
+  }
+  const int z[4] = {0, 0, 0, 0};
+  stage1_all<P>(w, r, 1.0, ca, cb, z);
+#if FMM_V4_STAGE_SYNC
+  __syncthreads();
+#endif
+  double h[2 * P + 1];  // Hankel entries k! / u^{k+1}
+  h[0] = iu;
+#pragma unroll
+  for (int k = 1; k <= 2 * P; ++k) h[k] = h[k - 1] * (k * iu);
+  stage2_all<P>(w, h);
+#if FMM_V4_STAGE_SYNC
+  __syncthreads();
+#endif
+  stage3_all<P>(w, ca, cb, z);
+}
+#endif
+
 template <int P>
 __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V4Args a) {
   using G = V4Geo<P>;
@@ -525,7 +568,10 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
       // geometry of the lane's pair (overlaps the copies)
       // (inactive lanes of a ragged chunk run the same code on the chunk's first pair and their
       // own stale rows — no divergence, results unused: the stages stay warp-uniform)
-      double2 ca[P + 1], cb[P + 1], e1, e2;
+      double2 e1, e2;
+#if !FMM_V4_CIMM
+      double2 ca[P + 1], cb[P + 1];
+#endif
       double r = 1.0, iu = 0.0;
       // (no IEEE division or sqrt here: their slow-path subroutine calls would force every
       // loop-carried value out of the uniform registers; rsqrt is inline)
@@ -547,6 +593,11 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
         }
         r = __hiloint2double((1023 + a.level[tgi] - a.level[sri]) << 20, 0);  // h_B / h_A = 2^{l_A - l_B}
       }
+#if FMM_V4_CIMM
+      cp_async_wait_all();
+      __syncwarp();
+      pair_transform<P>(w, r, e1, e2, iu);
+#else
       ca[0] = cb[0] = make_double2(1.0, 0.0);
       ca[1] = e1;
       cb[1] = e2;
@@ -578,6 +629,7 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
 #endif
         stage3_all<P>(w, ca, cb, z);
       }
+#endif
       __syncwarp();
       // 3. segmented sum over lanes with the same target: segments (runs of one target in the
       // target-grouped list) from a ballot; within a segment four interleaved partial sums

@@ -246,89 +246,117 @@ __global__ void __launch_bounds__(128) mutual_out_kernel(
   }
 }
 
+
+// setup, per entry k of the target-grouped P2P list (A = tgt[k], B = src[k]): the flags and sizes
+// the scans turn into the task lists, and the symmetry check — B's list must hold A exactly once
+// (that entry's index is kept for the reverse side: the task (B, A) when B < A).
+__global__ void mutual_mark_kernel(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src,
+                                   const int32_t* __restrict__ off, const int32_t* __restrict__ cb,
+                                   const int32_t* __restrict__ ce, int64_t np, int32_t* __restrict__ is_task,
+                                   int32_t* __restrict__ size, int32_t* __restrict__ is_rev,
+                                   int32_t* __restrict__ rpos, int* __restrict__ bad) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= np) return;
+  const int A = tgt[k], B = src[k];
+  int task = 0, sz = 0, rev = 0;
+  if (ce[A] - cb[A] > kMaxLeaf) atomicOr(bad, 1);
+  if (B != A) {
+    int j = -1, cnt = 0;
+    for (int i = off[B]; i < off[B + 1]; ++i)
+      if (src[i] == A) {
+        j = i;
+        ++cnt;
+      }
+    if (cnt != 1) atomicOr(bad, 2);
+    if (B > A) {
+      task = 1;
+      sz = ce[B] - cb[B];
+    } else {
+      rev = 1;
+      rpos[k] = j;
+    }
+  }
+  is_task[k] = task;
+  size[k] = sz;
+  is_rev[k] = rev;
+}
+
+// compaction: tasks (B, slot) in list order, the reverse side's slots in list order, and the
+// per-leaf offsets (a leaf's entries are off[A] .. off[A + 1]: the exclusive scans at off[A])
+__global__ void mutual_compact_kernel(const int32_t* __restrict__ src, int64_t np, const int32_t* __restrict__ is_task,
+                                      const int32_t* __restrict__ is_rev, const int32_t* __restrict__ rpos,
+                                      const int64_t* __restrict__ tscan, const int64_t* __restrict__ sscan,
+                                      const int64_t* __restrict__ rscan, int32_t* __restrict__ task_b,
+                                      int64_t* __restrict__ poff, int64_t* __restrict__ gslot) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= np) return;
+  if (is_task[k]) {
+    task_b[tscan[k]] = src[k];
+    poff[tscan[k]] = sscan[k];
+  } else if (is_rev[k]) {
+    gslot[rscan[k]] = sscan[rpos[k]];  // the slot of task (B, A) at its entry in B's list
+  }
+}
+
+__global__ void mutual_offsets_kernel(const int32_t* __restrict__ off, int64_t nc, int64_t np,
+                                      const int64_t* __restrict__ tscan, const int64_t* __restrict__ rscan,
+                                      int64_t ntasks, int64_t nrev, int32_t* __restrict__ toff,
+                                      int32_t* __restrict__ goff) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nc) return;
+  const int64_t o = c < nc ? off[c] : np;
+  toff[c] = (int32_t)(o < np ? tscan[o] : ntasks);
+  goff[c] = (int32_t)(o < np ? rscan[o] : nrev);
+}
+
 }  // namespace
 
-// host lists (setup): tasks (A, B > A) in A's list order, partial slots, and per leaf the slots of
-// the tasks where it is the B side. Disabled (directed path kept) if the lists are not symmetric, a
-// leaf exceeds kMaxLeaf particles, or the partial buffer would exceed 2 GB.
+// Task lists (setup, on the device): tasks (A, B > A) in A's list order with their partial slots,
+// and per leaf the slots of the tasks where it is the B side, in its list order. Disabled (the
+// directed path is kept) if the lists are not symmetric with each source at most once per list,
+// a leaf with pairs exceeds kMaxLeaf particles, or the partial buffer would exceed 2 GB.
 void near_mutual_setup(fmm_plan_s& P) {
   NearMutual& Mu = P.mutual;
   Mu.enabled = false;
   if (P.world != 1 || P.dim != 3 || P.helmholtz || P.p2p.n == 0) return;
   const int64_t nc = P.cells.n, np = P.p2p.n;
-  std::vector<int32_t> cb(nc), ce(nc), ps(np), off(nc + 1);
-  FMM_CUDA(cudaMemcpyAsync(cb.data(), P.cells.begin.ptr, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, P.stream));
-  FMM_CUDA(cudaMemcpyAsync(ce.data(), P.cells.end.ptr, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, P.stream));
-  FMM_CUDA(cudaMemcpyAsync(ps.data(), P.p2p.src.ptr, sizeof(int32_t) * np, cudaMemcpyDeviceToHost, P.stream));
-  FMM_CUDA(cudaMemcpyAsync(off.data(), P.p2p.off.ptr, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToHost,
-                           P.stream));
+  DevBuf<int32_t> is_task, size, is_rev, rpos;
+  DevBuf<int64_t> tscan, sscan, rscan;
+  DevBuf<int> bad;
+  is_task.alloc(np);
+  size.alloc(np);
+  is_rev.alloc(np);
+  rpos.alloc(np);
+  tscan.alloc(np);
+  sscan.alloc(np);
+  rscan.alloc(np);
+  bad.alloc(1);
+  FMM_CUDA(cudaMemsetAsync(bad.ptr, 0, sizeof(int), P.stream));
+  mutual_mark_kernel<<<cdiv(np, 256), 256, 0, P.stream>>>(P.p2p.tgt, P.p2p.src, P.p2p.off, P.cells.begin,
+                                                          P.cells.end, np, is_task, size, is_rev, rpos, bad);
+  FMM_LAUNCHED("mutual_mark_kernel");
+  const int64_t ntasks = scan_counts_total(is_task, tscan, np, P.stream);
+  const int64_t slots = scan_counts_total(size, sscan, np, P.stream);
+  const int64_t nrev = scan_counts_total(is_rev, rscan, np, P.stream);
+  int hbad = 0;
+  FMM_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost, P.stream));
   FMM_CUDA(cudaStreamSynchronize(P.stream));
-  for (int64_t c = 0; c < nc; ++c)
-    if (ce[c] - cb[c] > kMaxLeaf && off[c + 1] > off[c]) return;
-  // tasks: the pairs (A, B > A) of A's list, in list order; their keys (A, B) -> task index
-  std::vector<int32_t> toff(nc + 1, 0), tb;
-  std::vector<int64_t> poff;
-  std::vector<std::pair<uint64_t, int64_t>> fwd;  // (A << 32 | B, task)
-  std::vector<uint64_t> rev;                      // the pairs (L, A < L) as (A << 32 | L)
-  int64_t slots = 0;
-  for (int64_t A = 0; A < nc; ++A) {
-    toff[A] = (int32_t)tb.size();
-    for (int k = off[A]; k < off[A + 1]; ++k) {
-      const int64_t B = ps[k];
-      if (B > A) {
-        fwd.emplace_back((uint64_t)A << 32 | (uint64_t)B, (int64_t)tb.size());
-        tb.push_back((int32_t)B);
-        poff.push_back(slots);
-        slots += ce[B] - cb[B];
-      } else if (B < A) {
-        rev.push_back((uint64_t)B << 32 | (uint64_t)A);
-      }
-    }
-  }
-  toff[nc] = (int32_t)tb.size();
-  if (slots * 8 > ((int64_t)2 << 30)) return;
-  // symmetry: the two key sets are equal (each list holds a source at most once)
-  std::vector<std::pair<uint64_t, int64_t>> fs = fwd;
-  std::sort(fs.begin(), fs.end());
-  std::vector<uint64_t> rs = rev;
-  std::sort(rs.begin(), rs.end());
-  if (fs.size() != rs.size()) return;
-  for (size_t i = 0; i < fs.size(); ++i)
-    if (fs[i].first != rs[i] || (i > 0 && fs[i].first == fs[i - 1].first)) return;
-  // gather lists: for leaf L, the slots of the tasks (A, L) with A < L, in L's list order
-  std::vector<int32_t> goff(nc + 1, 0);
-  std::vector<int64_t> gslot;
-  gslot.reserve(rev.size());
-  size_t r = 0;
-  for (int64_t L = 0; L < nc; ++L) {
-    goff[L] = (int32_t)gslot.size();
-    for (int k = off[L]; k < off[L + 1]; ++k) {
-      if (ps[k] >= L) continue;
-      const uint64_t key = rev[r++];
-      const auto it = std::lower_bound(fs.begin(), fs.end(), std::make_pair(key, (int64_t)-1));
-      gslot.push_back(poff[it->second]);
-    }
-  }
-  goff[nc] = (int32_t)gslot.size();
-  auto up32 = [&](DevBuf<int32_t>& d, const std::vector<int32_t>& h) {
-    d.alloc(std::max<int64_t>(1, (int64_t)h.size()));
-    if (!h.empty())
-      FMM_CUDA(cudaMemcpyAsync(d.ptr, h.data(), sizeof(int32_t) * h.size(), cudaMemcpyHostToDevice, P.stream));
-  };
-  auto up64 = [&](DevBuf<int64_t>& d, const std::vector<int64_t>& h) {
-    d.alloc(std::max<int64_t>(1, (int64_t)h.size()));
-    if (!h.empty())
-      FMM_CUDA(cudaMemcpyAsync(d.ptr, h.data(), sizeof(int64_t) * h.size(), cudaMemcpyHostToDevice, P.stream));
-  };
-  up32(Mu.toff, toff);
-  up32(Mu.task_b, tb);
-  up64(Mu.poff, poff);
-  up32(Mu.goff, goff);
-  up64(Mu.gslot, gslot);
+  if (hbad || ntasks != nrev || slots * 8 > ((int64_t)2 << 30) || ntasks > INT32_MAX) return;
+  Mu.toff.alloc(nc + 1);
+  Mu.goff.alloc(nc + 1);
+  Mu.task_b.alloc(std::max<int64_t>(1, ntasks));
+  Mu.poff.alloc(std::max<int64_t>(1, ntasks));
+  Mu.gslot.alloc(std::max<int64_t>(1, nrev));
+  mutual_compact_kernel<<<cdiv(np, 256), 256, 0, P.stream>>>(P.p2p.src, np, is_task, is_rev, rpos, tscan, sscan,
+                                                             rscan, Mu.task_b, Mu.poff, Mu.gslot);
+  FMM_LAUNCHED("mutual_compact_kernel");
+  mutual_offsets_kernel<<<cdiv(nc + 1, 256), 256, 0, P.stream>>>(P.p2p.off, nc, np, tscan, rscan, ntasks, nrev,
+                                                                  Mu.toff, Mu.goff);
+  FMM_LAUNCHED("mutual_offsets_kernel");
   Mu.partial.alloc(std::max<int64_t>(1, slots));
   Mu.own.alloc(std::max<int64_t>(1, P.n));
-  Mu.ntasks = (int64_t)tb.size();
-  FMM_CUDA(cudaStreamSynchronize(P.stream));  // host vectors die here
+  Mu.ntasks = ntasks;
+  FMM_CUDA(cudaStreamSynchronize(P.stream));  // the scratch buffers die here
   Mu.enabled = true;
 }
 

@@ -79,10 +79,11 @@ def test_product_does_not_import_oracle():
 
 
 def test_m2l_v4_constants_stay_uniform():
-    """M2L v4 (csrc/m2l_v4.cu) reads its fixed operator as warp-uniform constant-bank loads (LDCU into
-    uniform registers, DFMA operands) once per use: no per-thread LDC (the ADU pipe throttled an
-    earlier build to 5 TFLOP/s), no spills, one copy of the pair code. A compiler-level property of
-    the built library, checked in its SASS."""
+    """M2L v4 (csrc/m2l_v4.cu) reads its fixed operator as warp-uniform constant-bank loads at immediate
+    addresses (LDCU.128 into uniform registers, DFMA operands) once per use: no per-thread LDC (the ADU
+    pipe throttled an earlier build to 5 TFLOP/s), one copy of the pair code in a called function
+    (FMM_V4_CIMM: the compiler cannot hoist its constants out of the chunk loop), no spills inside it.
+    A compiler-level property of the built library, checked in its SASS."""
     out = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_1602_02244_b200", "libfmm.so")],
                          capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s+Function : ", out)
@@ -90,6 +91,19 @@ def test_m2l_v4_constants_stay_uniform():
     assert len(body) == 1
     sass = body[0]
     assert len(re.findall(r"\bLDC(?:\.64)?\s+R\d+, c\[0x3\]", sass)) == 0
-    assert len(re.findall(r"\bLDCU(?:\.64|\.128)?\s+UR\d+, c\[0x3\]", sass)) > 1000
+    assert len(re.findall(r"\bLDCU\.128\s+UR\d+, c\[0x3\]\[0x[0-9a-f]+\]", sass)) > 800  # immediate, paired
+    assert len(re.findall(r"\bDFMA\b[^;]*UR\d+", sass)) >= 1804  # F, G, F^T, G^T: 4 x 451 at p = 10
     assert len(re.findall(r"\bDFMA\b", sass)) < 4000  # one copy of the ~3.2K-FMA pair code
-    assert "STL" not in sass  # no register spills
+    # the pair function: from the CALL target to its RET, free of local-memory traffic
+    ins = re.findall(r"/\*([0-9a-f]{4,})\*/\s+([^;]*);", sass)
+    targets = {int(t, 16) for t in re.findall(r"CALL\.REL\.NOINC (0x[0-9a-f]+)", sass)}
+    assert targets
+    t0 = min(targets)
+    fn = []
+    for a, txt in ins:
+        if int(a, 16) >= t0:
+            fn.append(txt)
+            if txt.strip().startswith("RET"):
+                break
+    assert sum("DFMA" in t for t in fn) > 3000
+    assert not any(re.match(r"\s*(STL|LDL)", t) for t in fn)  # no register spills in the pair code

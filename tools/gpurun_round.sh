@@ -14,5 +14,5 @@ python bench.py --config l3 --no-cpu-baseline --steps 5 > gpurun_out/bench_l3.lo
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-probe > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-probe > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:m2l_v4_kernel -s 1 -c 1 -o gpurun_out/m2l_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe > gpurun_out/ncu_m2l.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:near_warp -s 1 -c 1 -o gpurun_out/near_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe > gpurun_out/ncu_near.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:near_mutual_kernel -s 1 -c 1 -o gpurun_out/near_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe > gpurun_out/ncu_near.log 2>&1
 for f in gpurun_out/*.log; do echo "== $f"; tail -n 3 $f; done

@@ -11,11 +11,12 @@
 // L2P, the exact 2^-e rescale and the scatter to caller order. Every sum has a fixed order (no
 // atomics): bitwise deterministic.
 //
-// Lane layout per warp: 8 target groups x 4 source lanes. Lane (a, b) holds A's targets
-// i = a + 8k (k < TPL) in registers and takes the sources j = b + 4k' from shared memory. A's
+// Lane layout per warp: NG = 8 target groups x NS = 4 source lanes for leaves of <= 64 particles,
+// 16 x 2 above (<= 128). Lane (a, b) holds A's targets i = a + NG k (k < TPL = ceil(nA / NG)) in
+// registers and takes the sources j = b + NS k' from shared memory. A's
 // task sources (the B leaves, concatenated: their partial slots are contiguous) stream through
 // double-buffered cp.async units of kU particles. Per source j, a lane's partial over its
-// targets goes to a shared row red[a][j]; after the unit the 8 rows are summed in a fixed order
+// targets goes to a shared row red[a][j]; after the unit the NG rows are summed in a fixed order
 // (the B side). A's sums are reduced over the 4 source lanes at the end.
 // Per directed interaction: ~6 FP64 ops (12 per evaluated pair) instead of 11.
 #include <algorithm>
@@ -29,7 +30,8 @@
 namespace fmm {
 namespace {
 
-constexpr int kMaxLeaf = 64;  // particles per leaf (larger leaves: the directed path)
+constexpr int kMaxLeaf = 128;  // particles per leaf (larger leaves: the directed path)
+constexpr int kSmallLeaf = 64;  // up to here 8 target groups x 4 source lanes, above 16 x 2
 #ifndef FMM_MUTUAL_BUF
 #define FMM_MUTUAL_BUF 128
 #endif
@@ -63,10 +65,10 @@ struct MutualArgs {
 };
 
 // A's own leaf against itself: every ordered pair i != j (r^2 = 0 skipped: coincident points)
-template <int TPL>
+template <int NS, int TPL>
 __device__ __forceinline__ void self_unit(const double4* __restrict__ sbuf, int n, int b, const double3 (&xi)[TPL],
                                           double (&fi)[TPL]) {
-  for (int j = b; j < n; j += 4) {
+  for (int j = b; j < n; j += NS) {
     const double4 s = sbuf[j];
 #pragma unroll
     for (int k = 0; k < TPL; ++k) {
@@ -81,11 +83,12 @@ __device__ __forceinline__ void self_unit(const double4* __restrict__ sbuf, int 
 // n sources of other leaves: 1/r once per pair, q_j / r to A's sums (registers), q_i / r to the
 // source's B-side sum (this lane's partial over its TPL targets to red[a][j], then summed over
 // the 8 target groups in a fixed order and stored to the task's partial slots)
-template <int TPL>
+template <int NG, int TPL>
 __device__ __forceinline__ void mutual_unit(const double4* __restrict__ sbuf, int n, int a, int b, int lane,
                                             const double3 (&xi)[TPL], const double (&qi)[TPL], double (&fi)[TPL],
                                             double* __restrict__ red, double* __restrict__ out) {
-  for (int j0 = 0; j0 < n; j0 += 4) {  // j < 4 ceil(n / 4) <= kR
+  constexpr int NS = 32 / NG;
+  for (int j0 = 0; j0 < n; j0 += NS) {  // j < NS ceil(n / NS) <= kR
     const int j = j0 + b;
     double4 s = sbuf[j < n ? j : 0];    // padding sources: source 0 with charge 0
     if (j >= n) s.w = 0.0;
@@ -104,7 +107,7 @@ __device__ __forceinline__ void mutual_unit(const double4* __restrict__ sbuf, in
   for (int j = lane; j < n; j += 32) {
     double t = red[j];
 #pragma unroll
-    for (int g = 1; g < 8; ++g) t += red[g * kR + j];
+    for (int g = 1; g < NG; ++g) t += red[g * kR + j];
     out[j] = t;
   }
 }
@@ -115,15 +118,16 @@ struct Span {
   int64_t base;  // stream offset of the unit (partial slot - poff[t0])
 };
 
-template <int TPL>
+template <int NG, int TPL>
 __device__ void mutual_leaf(const MutualArgs& m, int A, int lane, double4 (*buf)[kU], double* red) {
-  const int a = lane >> 2, b = lane & 3;
+  constexpr int NS = 32 / NG;
+  const int a = lane / NS, b = lane % NS;
   const int ab = m.cbeg[A], nA = m.cend[A] - ab;
   double3 xi[TPL];
   double qi[TPL], fi[TPL];
 #pragma unroll
   for (int k = 0; k < TPL; ++k) {
-    const int i = a + 8 * k;
+    const int i = a + NG * k;
     // padding targets: copies of target 0 with charge 0 (a point of A: r > 0 to every point of B)
     const double4 v = m.pos[ab + (i < nA ? i : 0)];
     xi[k] = make_double3(v.x, v.y, v.z);
@@ -185,40 +189,56 @@ __device__ void mutual_leaf(const MutualArgs& m, int A, int lane, double4 (*buf)
     }
     __syncwarp();
     if (cur.base < 0)
-      self_unit<TPL>(buf[bb], cur.n, b, xi, fi);
+      self_unit<NS, TPL>(buf[bb], cur.n, b, xi, fi);
     else
-      mutual_unit<TPL>(buf[bb], cur.n, a, b, lane, xi, qi, fi, red, out0 + cur.base);
+      mutual_unit<NG, TPL>(buf[bb], cur.n, a, b, lane, xi, qi, fi, red, out0 + cur.base);
     __syncwarp();  // buffer bb and red are rewritten by the next units
     if (!more) break;
     cur = nx;
     bb ^= 1;
   }
-  // A side: sum over the 4 source lanes
+  // A side: sum over the NS source lanes
 #pragma unroll
   for (int k = 0; k < TPL; ++k) {
-    fi[k] += __shfl_xor_sync(0xffffffffu, fi[k], 1);
-    fi[k] += __shfl_xor_sync(0xffffffffu, fi[k], 2);
-    const int i = a + 8 * k;
+#pragma unroll
+    for (int o = 1; o < NS; o <<= 1) fi[k] += __shfl_xor_sync(0xffffffffu, fi[k], o);
+    const int i = a + NG * k;
     if (b == 0 && i < nA) m.own[ab + i] = fi[k];
   }
 }
 
+// NGMAX = 8: every leaf <= kSmallLeaf particles; 16: larger leaves too (twice the B-side rows)
+template <int NGMAX>
 __global__ void __launch_bounds__(32, FMM_MUTUAL_MINB) near_mutual_kernel(const MutualArgs m) {
   __shared__ __align__(16) double4 buf[2][kU];
-  __shared__ double red[8 * kR];
+  __shared__ double red[NGMAX * kR];
   const int64_t li = blockIdx.x;
   if (li >= m.nleaves) return;
   const int A = m.leaves[li];
   const int nA = m.cend[A] - m.cbeg[A];
   const int lane = threadIdx.x & 31;
-  if (nA <= 8)
-    mutual_leaf<1>(m, A, lane, buf, red);
-  else if (nA <= 16)
-    mutual_leaf<2>(m, A, lane, buf, red);
-  else if (nA <= 32)
-    mutual_leaf<4>(m, A, lane, buf, red);
-  else
-    mutual_leaf<8>(m, A, lane, buf, red);
+  // TPL = ceil(nA / 8): idle target slots < 8 per leaf (powers of two only left 30 % of the
+  // lanes idle on the Poisson(30.5) leaves of configs[2]); leaves above 64: 16 x 2 lanes
+  if (NGMAX == 16 && nA > kSmallLeaf) {
+    switch ((nA + 15) >> 4) {
+      case 5: mutual_leaf<16, 5>(m, A, lane, buf, red); break;
+      case 6: mutual_leaf<16, 6>(m, A, lane, buf, red); break;
+      case 7: mutual_leaf<16, 7>(m, A, lane, buf, red); break;
+      default: mutual_leaf<16, 8>(m, A, lane, buf, red); break;
+    }
+    return;
+  }
+  switch ((nA + 7) >> 3) {
+    case 0:
+    case 1: mutual_leaf<8, 1>(m, A, lane, buf, red); break;
+    case 2: mutual_leaf<8, 2>(m, A, lane, buf, red); break;
+    case 3: mutual_leaf<8, 3>(m, A, lane, buf, red); break;
+    case 4: mutual_leaf<8, 4>(m, A, lane, buf, red); break;
+    case 5: mutual_leaf<8, 5>(m, A, lane, buf, red); break;
+    case 6: mutual_leaf<8, 6>(m, A, lane, buf, red); break;
+    case 7: mutual_leaf<8, 7>(m, A, lane, buf, red); break;
+    default: mutual_leaf<8, 8>(m, A, lane, buf, red); break;
+  }
 }
 
 // own + the partials of the tasks where the leaf is the B side (list order), then L2P, the exact
@@ -260,6 +280,7 @@ __global__ void mutual_mark_kernel(const int32_t* __restrict__ tgt, const int32_
   const int A = tgt[k], B = src[k];
   int task = 0, sz = 0, rev = 0;
   if (ce[A] - cb[A] > kMaxLeaf) atomicOr(bad, 1);
+  if (ce[A] - cb[A] > kSmallLeaf) atomicOr(bad, 4);  // (not a failure: the 16-group kernel)
   if (B != A) {
     int j = -1, cnt = 0;
     for (int i = off[B]; i < off[B + 1]; ++i)
@@ -314,7 +335,8 @@ __global__ void mutual_offsets_kernel(const int32_t* __restrict__ off, int64_t n
 // Task lists (setup, on the device): tasks (A, B > A) in A's list order with their partial slots,
 // and per leaf the slots of the tasks where it is the B side, in its list order. Disabled (the
 // directed path is kept) if the lists are not symmetric with each source at most once per list,
-// a leaf with pairs exceeds kMaxLeaf particles, or the partial buffer would exceed 2 GB.
+// a leaf with pairs exceeds kMaxLeaf particles, or the partial buffer would take more than a
+// quarter of the free device memory.
 void near_mutual_setup(fmm_plan_s& P) {
   NearMutual& Mu = P.mutual;
   Mu.enabled = false;
@@ -341,7 +363,11 @@ void near_mutual_setup(fmm_plan_s& P) {
   int hbad = 0;
   FMM_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost, P.stream));
   FMM_CUDA(cudaStreamSynchronize(P.stream));
-  if (hbad || ntasks != nrev || slots * 8 > ((int64_t)2 << 30) || ntasks > INT32_MAX) return;
+  Mu.big = (hbad & 4) != 0;
+  hbad &= 3;
+  size_t mem_free = 0, mem_total = 0;
+  FMM_CUDA(cudaMemGetInfo(&mem_free, &mem_total));
+  if (hbad || ntasks != nrev || (size_t)slots * 8 > mem_free / 4 || ntasks > INT32_MAX) return;
   Mu.toff.alloc(nc + 1);
   Mu.goff.alloc(nc + 1);
   Mu.task_b.alloc(std::max<int64_t>(1, ntasks));
@@ -376,7 +402,10 @@ void near_mutual_pass(fmm_plan_s& P, double* phi) {
   m.poff = Mu.poff;
   m.partial = Mu.partial;
   m.own = Mu.own;
-  near_mutual_kernel<<<(unsigned)nl, 32, 0, P.stream>>>(m);
+  if (Mu.big)
+    near_mutual_kernel<16><<<(unsigned)nl, 32, 0, P.stream>>>(m);
+  else
+    near_mutual_kernel<8><<<(unsigned)nl, 32, 0, P.stream>>>(m);
   FMM_LAUNCHED("near_mutual_kernel");
   mutual_out_kernel<<<cdiv(nl, 4), 128, 0, P.stream>>>(leaves, nl, P.cells.begin, P.cells.end, P.cells.center,
                                                        P.pos, P.L, P.p, P.nc, Mu.own, Mu.goff, Mu.gslot, Mu.partial,

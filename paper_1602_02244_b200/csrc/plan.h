@@ -120,6 +120,7 @@ struct M2L4 {
 // mutual near field (near_mutual.cu): each unordered leaf pair evaluated once, single GPU, potentials
 struct NearMutual {
   bool enabled = false;
+  bool big = false;  // a leaf with pairs has more than 64 particles (16 target groups x 2 source lanes)
   DevBuf<int32_t> toff, task_b;  // tasks (A, B > A) grouped by A: [ncells + 1], [ntasks]
   DevBuf<int64_t> poff;          // [ntasks] B-side partial slot
   DevBuf<int32_t> goff;          // [ncells + 1] per leaf, its B-side slots (gslot) in list order

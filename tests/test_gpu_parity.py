@@ -435,7 +435,8 @@ def test_repeated_matvecs_bitwise_equal(torch_cuda, monkeypatch):
 
 @pytest.mark.parametrize("dist,n,p,ncrit,theta", [("cube", 30000, 10, 64, 0.4), ("plummer", 20000, 6, 32, 0.5),
                                                   ("sphere", 20000, 8, 16, 0.4), ("plummer", 8000, 3, 7, 0.3),
-                                                  ("cube", 3000, 2, 16, 1e-6), ("cube", 4000, 4, 1, 0.4)])
+                                                  ("cube", 3000, 2, 16, 1e-6), ("cube", 4000, 4, 1, 0.4),
+                                                  ("sphere", 40000, 12, 128, 0.4), ("cube", 20000, 6, 100, 0.4)])
 def test_mutual_near_field(torch_cuda, monkeypatch, dist, n, p, ncrit, theta):
     """Potentials-only mat-vecs evaluate each unordered P2P leaf pair once (csrc/near_mutual.cu):
     oracle parity, agreement with the directed P2P (FMM_NEAR_MUTUAL=0) to rounding, and bitwise
@@ -465,11 +466,19 @@ def test_mutual_near_field(torch_cuda, monkeypatch, dist, n, p, ncrit, theta):
 
 
 def test_mutual_near_field_limits(torch_cuda):
-    """Leaves above 64 particles keep the directed P2P (the mutual kernel's register layout)."""
+    """Leaves above 128 particles keep the directed P2P (the mutual kernel's register layout);
+    leaves of 65-128 take its 16-group layout, checked against the directed path."""
     torch = torch_cuda
     from paper_1602_02244_b200 import Plan
 
-    x, q = F.make("cube", 8000)  # 8000 / 64 = 125 per level-2 cell: leaves of ~125 particles
-    pl = Plan(to_dev(torch, x), 4, 200, 0.4)
+    x, q = F.make("cube", 16000)  # 16000 / 64 = 250 per level-2 cell: leaves of ~250 particles
+    pl = Plan(to_dev(torch, x), 4, 300, 0.4)
     assert pl.stats()["near_mutual"] == 0
-    assert pl.matvec(to_dev(torch, q)).shape == (8000,)
+    assert pl.matvec(to_dev(torch, q)).shape == (16000,)
+    x, q = F.make("cube", 8000)  # 8000 / 64 = 125 per level-2 cell: leaves of ~125 particles
+    xd, qd = to_dev(torch, x), to_dev(torch, q)
+    pl = Plan(xd, 4, 128, 0.4)  # leaves of <= 128, most of them above 64
+    assert pl.stats()["near_mutual"] == 1
+    phi = pl.matvec(qd).cpu().numpy()
+    po = O.fmm(x, q, 4, 128, 0.4)
+    assert O.rel_l2(phi, po) <= 1e-11

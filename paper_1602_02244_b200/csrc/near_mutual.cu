@@ -32,12 +32,16 @@ namespace {
 
 constexpr int kMaxLeaf = 128;  // particles per leaf (larger leaves: the directed path)
 constexpr int kSmallLeaf = 64;  // up to here 8 target groups x 4 source lanes, above 16 x 2
+#ifndef FMM_MUTUAL_UNROLL
+#define FMM_MUTUAL_UNROLL 1  // source-loop unroll of the mutual units
+#endif
 #ifndef FMM_MUTUAL_BUF
 #define FMM_MUTUAL_BUF 128
 #endif
 #ifndef FMM_MUTUAL_MINB
 #define FMM_MUTUAL_MINB 12  // warps (CTAs) per SM: 16.4 KB shared memory each
 #endif
+constexpr int kUnroll = FMM_MUTUAL_UNROLL;
 constexpr int kU = FMM_MUTUAL_BUF;  // source particles per staged unit
 constexpr int kR = kU + 4;          // row stride of the B-side partials: 2 wavefronts per store
 
@@ -88,6 +92,7 @@ __device__ __forceinline__ void mutual_unit(const double4* __restrict__ sbuf, in
                                             const double3 (&xi)[TPL], const double (&qi)[TPL], double (&fi)[TPL],
                                             double* __restrict__ red, double* __restrict__ out) {
   constexpr int NS = 32 / NG;
+#pragma unroll kUnroll
   for (int j0 = 0; j0 < n; j0 += NS) {  // j < NS ceil(n / NS) <= kR
     const int j = j0 + b;
     double4 s = sbuf[j < n ? j : 0];    // padding sources: source 0 with charge 0

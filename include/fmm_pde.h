@@ -71,6 +71,51 @@ typedef struct {
 FMM_API fmm_status fmm_pcg_solve(int n, const double* b, double* x, fmm_precond M, double rtol, int maxit,
                                  double* hist, fmm_pcg_info* info, void* stream);
 
+/*
+ * NEXT-4 solve: the Helmholtz equation -Delta u - kappa^2 u = f on the same
+ * lattice with Dirichlet faces, the Helmholtz FMM of include/fmm_helmholtz.h as the preconditioner
+ * inside GMRES ("the Laplace equation and Helmholtz equation on a 3D cubic lattice [-1,1]^3 [...]
+ * The preconditioners are used inside a Krylov subspace solver"; Fig 6, kappa = 7
+ * at h = 2^-5). Readings (R56-R60), those above with:
+ *   operator  A = -Delta_h - kappa^2 I (real symmetric, indefinite for kappa = 7);
+ *   G         exp(i kappa r) / (4 pi r); own-cell integral c_self = h^2 C_cube / (4 pi)
+ *             + i kappa h^3 / (4 pi), own-panel S_ii = a C_panel / (4 pi) + i kappa a^2 / (4 pi);
+ *             S complex symmetric, S^-1 by complex Newton-Schulz (cuBLAS ZGEMM) at setup;
+ *   Krylov    GMRES, right preconditioned (x = M u), x0 = 0, no restart, Arnoldi by classical
+ *             Gram-Schmidt with one re-orthogonalisation, Givens rotations; stop when the residual
+ *             estimate |g_{k+1}| / ||b|| <= rtol.
+ * Complex vectors are interleaved (re, im) doubles: [n^3][2] (a torch complex128 tensor).
+ */
+typedef struct fmm_hprecond_s* fmm_hprecond; /* opaque */
+
+/* out = (-Delta_h - kappa^2) u on the n^3 lattice; u, out: device [n^3][2], distinct. Stream
+ * ordered on `stream`. USAGE for n < 1, n^3 >= 2^30, non-finite kappa, NULL/aliased pointers. */
+FMM_API fmm_status fmm_helmholtz_stencil_apply(int n, double kappa, const double* u, double* out, void* stream);
+
+/* Precalculation of the Helmholtz M (as fmm_precond_setup; kappa > 0 finite; p <= 10 as
+ * fmm_setup_helmholtz). Synchronises ex->stream. Errors: USAGE, NUMERIC (Newton-Schulz did not
+ * converge: S singular or too ill-conditioned, e.g. kappa^2 at an interior Dirichlet eigenvalue),
+ * CUDA, OOM. */
+FMM_API fmm_status fmm_hprecond_setup(fmm_hprecond* out, int n, int face_stride, int p, int ncrit, double theta,
+                                      double kappa, int boundary, const fmm_exec* ex);
+
+/* z = M r; r, z: device [n^3][2] complex, distinct. Stream ordered (ex->stream of setup). */
+FMM_API fmm_status fmm_hprecond_apply(fmm_hprecond P, const double* r, double* z);
+
+/* Panel count and the device memory owned by M (bytes). Either pointer may be NULL. */
+FMM_API fmm_status fmm_hprecond_info(fmm_hprecond P, int64_t* n_panels, int64_t* bytes);
+
+FMM_API void fmm_hprecond_destroy(fmm_hprecond P);
+
+/* Solve (-Delta_h - kappa^2) x = b by GMRES with M (NULL = identity). b, x: device [n^3][2]
+ * complex; hist: host [maxit + 1] residual estimates (history[0] = 1) or NULL; info may be NULL
+ * (t_precond_ms: time inside M). Synchronous (one host read per Gram-Schmidt pass). Device
+ * memory: (maxit + 1) n^3 complex basis vectors. M must have been set up for the same n and
+ * kappa. Errors: USAGE (n, kappa, rtol <= 0, maxit < 0, mismatch with M), NUMERIC (non-finite
+ * values), CUDA, OOM. */
+FMM_API fmm_status fmm_gmres_solve(int n, double kappa, const double* b, double* x, fmm_hprecond M, double rtol,
+                                   int maxit, double* hist, fmm_pcg_info* info, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,7 +24,8 @@ EXPORTED = ("fmm_setup", "fmm_setup_2d", "fmm_matvec", "fmm_matvec_host", "fmm_s
             "fmm_let_counts", "fmm_let_pack_q", "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack",
             "fmm_let_lists_host", "fmm_stencil_apply", "fmm_precond_setup", "fmm_precond_apply", "fmm_precond_info",
             "fmm_precond_destroy", "fmm_pcg_solve", "fmm_nccl_unique_id", "fmm_setup_helmholtz",
-            "fmm_matvec_helmholtz", "fmm_direct_helmholtz")
+            "fmm_matvec_helmholtz", "fmm_direct_helmholtz", "fmm_helmholtz_stencil_apply", "fmm_hprecond_setup",
+            "fmm_hprecond_apply", "fmm_hprecond_info", "fmm_hprecond_destroy", "fmm_gmres_solve")
 
 
 class FmmExec(C.Structure):
@@ -106,6 +107,19 @@ def lib() -> C.CDLL:
     L.fmm_precond_destroy.restype = None
     L.fmm_pcg_solve.argtypes = [C.c_int, dp, dp, vp, C.c_double, C.c_int, C.POINTER(C.c_double),
                                 C.POINTER(PcgInfo), vp]
+    # include/fmm_pde.h, NEXT-4 solve (Helmholtz, GMRES)
+    L.fmm_helmholtz_stencil_apply.argtypes = [C.c_int, C.c_double, dp, dp, vp]
+    L.fmm_hprecond_setup.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                     C.c_int, C.POINTER(FmmExec)]
+    L.fmm_hprecond_apply.argtypes = [vp, dp, dp]
+    L.fmm_hprecond_info.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.fmm_hprecond_destroy.argtypes = [vp]
+    L.fmm_hprecond_destroy.restype = None
+    L.fmm_gmres_solve.argtypes = [C.c_int, C.c_double, dp, dp, vp, C.c_double, C.c_int, C.POINTER(C.c_double),
+                                  C.POINTER(PcgInfo), vp]
+    for nm in ("fmm_helmholtz_stencil_apply", "fmm_hprecond_setup", "fmm_hprecond_apply", "fmm_hprecond_info",
+               "fmm_gmres_solve"):
+        getattr(L, nm).restype = C.c_int
     for nm in ("fmm_setup", "fmm_setup_2d", "fmm_matvec", "fmm_matvec_host", "fmm_sync", "fmm_direct", "fmm_stats",
                "fmm_set_timing", "fmm_export", "fmm_let_setup", "fmm_let_counts", "fmm_let_pack_q",
                "fmm_let_upward", "fmm_let_finish", "fmm_let_unpack", "fmm_let_lists_host", "fmm_nccl_unique_id",

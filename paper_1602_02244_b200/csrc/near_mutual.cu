@@ -21,6 +21,7 @@
 // Per directed interaction: ~6 FP64 ops (12 per evaluated pair) instead of 11.
 #include <algorithm>
 #include <cmath>
+#include <utility>
 #include <vector>
 
 #include "harmonics.cuh"
@@ -246,31 +247,82 @@ __global__ void __launch_bounds__(32, FMM_MUTUAL_MINB) near_mutual_kernel(const 
   }
 }
 
+// L2P of the potential at (x, y, z) from a cell's local expansion in shared memory, degree P known
+// at compile time (the recurrences of harmonics.cuh l2p_eval in the same order)
+template <int P>
+__device__ __forceinline__ double l2p_phi(const double2* __restrict__ Ls, double x, double y, double z) {
+  const double r2 = x * x + y * y + z * z;
+  double2 diag = make_double2(1.0, 0.0);
+  double f = 0.0;
+#pragma unroll 1
+  for (int m = 0; m <= P; ++m) {
+    if (m > 0) {
+      const double s = c_half_inv.v[m];
+      diag = cmul(diag, make_double2(s * x, s * y));
+    }
+    const double w = m == 0 ? 1.0 : 2.0;
+    double2 a = make_double2(0, 0), b = diag;  // R_{n-1}^m, R_n^m
+#pragma unroll 4
+    for (int n = m; n <= P; ++n) {
+      if (n == m + 1) {
+        a = b;
+        b = cscale(diag, z);
+      } else if (n > m + 1) {
+        const double inv = c_inv_nm.v[n * (kMaxP + 1) + m];
+        const double2 c = make_double2(((2 * n - 1) * z * b.x - r2 * a.x) * inv, ((2 * n - 1) * z * b.y - r2 * a.y) * inv);
+        a = b;
+        b = c;
+      }
+      const double2 l = Ls[cidx(n, m)];
+      f += w * (l.x * b.x + l.y * b.y);
+    }
+  }
+  return f;
+}
+
 // own + the partials of the tasks where the leaf is the B side (list order), then L2P, the exact
-// rescale and the scatter (warp per leaf, lane per target)
+// rescale and the scatter (warp per leaf, lane per target; the leaf's local expansion staged in
+// shared memory once per warp)
+template <int P>
 __global__ void __launch_bounds__(128) mutual_out_kernel(
     const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ cbeg,
     const int32_t* __restrict__ cend, const double4* __restrict__ center, const double4* __restrict__ pos,
-    const double2* __restrict__ L, int p, int nc, const double* __restrict__ own, const int32_t* __restrict__ goff,
+    const double2* __restrict__ L, const double* __restrict__ own, const int32_t* __restrict__ goff,
     const int64_t* __restrict__ gslot, const double* __restrict__ partial, const uint32_t* __restrict__ perm,
     double s_phi, double* __restrict__ phi_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t li = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  constexpr int NC = (P + 1) * (P + 2) / 2;
+  __shared__ double2 Lsh[4][NC];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int64_t li = (int64_t)blockIdx.x * 4 + wi;
   if (li >= nleaves) return;
   const int leaf = leaves[li];
   const double4 c = center[leaf];
-  const double2* Lc = L + (int64_t)leaf * nc;
+  const double2* Lc = L + (int64_t)leaf * NC;
+  for (int k = lane; k < NC; k += 32) Lsh[wi][k] = Lc[k];
+  __syncwarp();
   const int tb = cbeg[leaf], g0 = goff[leaf], g1 = goff[leaf + 1];
   for (int t = tb + lane; t < cend[leaf]; t += 32) {
     const double4 x = pos[t];
     double f = own[t];
     for (int g = g0; g < g1; ++g) f += partial[gslot[g] + (t - tb)];
-    double3 gr = make_double3(0, 0, 0);
-    l2p_eval<false>(Lc, p, x.x - c.x, x.y - c.y, x.z - c.z, f, gr);
+    f += l2p_phi<P>(Lsh[wi], x.x - c.x, x.y - c.y, x.z - c.z);
     phi_out[perm[t]] = f * s_phi;
   }
 }
 
+template <int P>
+void launch_mutual_out(const fmm_plan_s& Pl, const NearMutual& Mu, const int32_t* leaves, int64_t nl, double* phi) {
+  mutual_out_kernel<P><<<cdiv(nl, 4), 128, 0, Pl.stream>>>(leaves, nl, Pl.cells.begin, Pl.cells.end, Pl.cells.center,
+                                                          Pl.pos, Pl.L, Mu.own, Mu.goff, Mu.gslot, Mu.partial, Pl.perm,
+                                                          std::ldexp(1.0, -Pl.e), phi);
+}
+template <int... Ps>
+void dispatch_mutual_out(int p, const fmm_plan_s& Pl, const NearMutual& Mu, const int32_t* leaves, int64_t nl,
+                         double* phi, std::integer_sequence<int, Ps...>) {
+  bool done = false;
+  ((p == Ps ? (launch_mutual_out<Ps>(Pl, Mu, leaves, nl, phi), done = true) : false), ...);
+  if (!done) throw Error(FMM_ERR_USAGE, "near_mutual: p out of range");
+}
 
 // setup, per entry k of the target-grouped P2P list (A = tgt[k], B = src[k]): the flags and sizes
 // the scans turn into the task lists, and the symmetry check — B's list must hold A exactly once
@@ -412,9 +464,7 @@ void near_mutual_pass(fmm_plan_s& P, double* phi) {
   else
     near_mutual_kernel<8><<<(unsigned)nl, 32, 0, P.stream>>>(m);
   FMM_LAUNCHED("near_mutual_kernel");
-  mutual_out_kernel<<<cdiv(nl, 4), 128, 0, P.stream>>>(leaves, nl, P.cells.begin, P.cells.end, P.cells.center,
-                                                       P.pos, P.L, P.p, P.nc, Mu.own, Mu.goff, Mu.gslot, Mu.partial,
-                                                       P.perm, std::ldexp(1.0, -P.e), phi);
+  dispatch_mutual_out(P.p, P, Mu, leaves, nl, phi, std::make_integer_sequence<int, kMaxP + 1>{});
   FMM_LAUNCHED("mutual_out_kernel");
 }
 

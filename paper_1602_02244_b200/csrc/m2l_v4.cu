@@ -314,11 +314,47 @@ __device__ __forceinline__ void apply_seq(const double (&x)[2 * N + 1], double (
 // z: a run-time zero the compiler cannot see (zmask = 0), different per call site and per chunk
 // and warp-uniform: the constants are loaded (LDCU, uniform datapath) right where they are used,
 // never held in registers across pairs or shared between the stages
+// FMM_V4_ORDER = 1 (default; configs[2] M2L 3.00 -> 2.96 ms): the entries in output-interleaved order (for y = F x sorted by input column,
+// for y = F^T x by row), so consecutive FMAs go to different accumulators (the table of constants
+// is unchanged: an entry keeps its index I; each accumulator sums in the same order as before, so the
+// results are bitwise the same)
+#ifndef FMM_V4_ORDER
+#define FMM_V4_ORDER 1
+#endif
+template <int N, bool T>
+struct FOrder {
+  int v[nnzF(N)];
+};
+template <int N, bool T>
+constexpr FOrder<N, T> make_forder() {
+  FOrder<N, T> o{};
+  int j = 0;
+  // output index of entry I is e.r (F) or e.k (F^T); its input index the other one
+  for (int in = 0; in < 2 * N + 1; ++in)
+    for (int I = 0; I < nnzF(N); ++I) {
+      const FEnt e = FTabOf<N>::value.e[I];
+      if ((T ? e.r : e.k) == in) o.v[j++] = I;
+    }
+  return o;
+}
+template <int N, bool T>
+struct FOrderOf {
+  static constexpr FOrder<N, T> value = make_forder<N, T>();
+};
+template <int N, bool T, bool SG, bool SX, int... J>
+__device__ __forceinline__ void apply_perm(const double (&x)[2 * N + 1], double (&y)[2 * N + 1], int z,
+                                           std::integer_sequence<int, J...>) {
+  (fstep<N, T, SG, SX, FOrderOf<N, T>::value.v[J]>(x, y, z), ...);
+}
 template <int N, bool T, bool SG, bool SX>
 __device__ __forceinline__ void apply_fixed(const double (&x)[2 * N + 1], double (&y)[2 * N + 1], int z) {
 #pragma unroll
   for (int i = 0; i < 2 * N + 1; ++i) y[i] = 0.0;
+#if FMM_V4_ORDER
+  apply_perm<N, T, SG, SX>(x, y, z, std::make_integer_sequence<int, nnzF(N)>{});
+#else
   apply_seq<N, T, SG, SX>(x, y, z, std::make_integer_sequence<int, nnzF(N)>{});
+#endif
 }
 
 // (re, im) of order m -> e^{i m t} (re + i im), m = 1..N; cs[m] = (cos mt, sin mt)

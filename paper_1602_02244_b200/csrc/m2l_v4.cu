@@ -60,7 +60,9 @@ namespace fmm {
 namespace m2l4 {
 
 constexpr int kMinP = 2, kMaxP4 = 12;  // orders served by v4 (others: v3 / v2)
-constexpr int kUnitChunks = 16;        // default chunks of 32 pairs per work unit (balanced at launch)
+constexpr int kUnitChunks = 4;         // chunks of 32 pairs per work unit (balanced at setup); 16 -> 4:
+                                       // a CTA's warps on adjacent targets share source rows in L1
+                                       // (configs[2] M2L 2.96 -> 2.78 ms, configs[3] 20.9 -> 19.8 ms)
 constexpr int kMaxWarpsPerCta = 8;     // M2L v4 CTA: up to 8 one-warp workers
 
 
@@ -318,6 +320,9 @@ __device__ __forceinline__ void apply_seq(const double (&x)[2 * N + 1], double (
 // for y = F^T x by row), so consecutive FMAs go to different accumulators (the table of constants
 // is unchanged: an entry keeps its index I; each accumulator sums in the same order as before, so the
 // results are bitwise the same)
+#ifndef FMM_V4_S2ORDER
+#define FMM_V4_S2ORDER 0  // stage 2 (Hankel) FMAs output-interleaved (measured neutral)
+#endif
 #ifndef FMM_V4_ORDER
 #define FMM_V4_ORDER 1
 #endif
@@ -390,6 +395,20 @@ __device__ __forceinline__ void stage2(double* w, const double* h) {
   double a[L], y[L];
 #pragma unroll
   for (int i = 0; i < L; ++i) a[i] = w[(M + i) * (M + i) + ridx(M, PART)];
+#if FMM_V4_S2ORDER
+  // n outer, j inner: consecutive FMAs to different outputs (each output sums over n in the same
+  // order as below: bitwise the same)
+#pragma unroll
+  for (int j = 0; j < L; ++j) y[j] = 0.0;
+#pragma unroll
+  for (int n = 0; n < L; ++n)
+#pragma unroll
+    for (int j = 0; j < L; ++j) y[j] = fma(h[2 * M + j + n], a[n], y[j]);
+  if (M == 0) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) y[j] *= 0.5;
+  }
+#else
 #pragma unroll
   for (int j = 0; j < L; ++j) {
     double s = 0.0;
@@ -397,6 +416,7 @@ __device__ __forceinline__ void stage2(double* w, const double* h) {
     for (int n = 0; n < L; ++n) s = fma(h[2 * M + j + n], a[n], s);
     y[j] = M == 0 ? 0.5 * s : s;
   }
+#endif
 #pragma unroll
   for (int i = 0; i < L; ++i) w[(M + i) * (M + i) + ridx(M, PART)] = y[i];
 }

@@ -246,6 +246,8 @@ void let_finish_impl(fmm_plan_s& P, const double* shared_recv, const double* m_r
   P.near_compact_out = true;
   if (P.near_fused_active)
     fmm::near_fused_finish(P, P.let_dev.phi_own.ptr, grad_send ? P.let_dev.grad_own.ptr : nullptr);
+  else if (P.mutual.enabled && !grad_send)
+    fmm::near_mutual_pass(P, P.let_dev.phi_own.ptr);
   else
     fmm::near_pass_warp(P, P.let_dev.phi_own.ptr, grad_send ? P.let_dev.grad_own.ptr : nullptr);
   P.near_compact_out = false;
@@ -431,7 +433,7 @@ fmm_status setup_impl(fmm_plan* out, const double* xyz, int64_t n, int p, int nc
         fmm::m2l_dmma_setup(*P);
       fmm::shift_setup(*P);
       const char* mu = getenv("FMM_NEAR_MUTUAL");  // 0: directed P2P for potentials too
-      if (P->near_variant == 2 && !collective && P->world == 1 && !(mu && mu[0] == '0'))
+      if (P->near_variant == 2 && !(mu && mu[0] == '0'))  // (world > 1: mutual among this rank's leaves)
         fmm::near_mutual_setup(*P);
     }
     P->M.alloc(P->cells.n * P->nc);

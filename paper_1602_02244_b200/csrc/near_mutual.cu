@@ -63,6 +63,7 @@ struct MutualArgs {
   const int32_t *cbeg, *cend;
   const double4* pos;       // x, y, z, q (Morton order)
   const int32_t* toff;      // [ncells + 1] tasks of leaf A: (A, task_b[t]) for t in [toff[A], toff[A+1])
+  const int32_t* tmend;     // [ncells] tasks [toff[A], tmend[A]) are mutual, the rest directed (B not owned)
   const int32_t* task_b;
   const int64_t* poff;      // [ntasks] partial slot of task t (|B| doubles; contiguous over A's tasks)
   double* partial;          // B-side sums
@@ -121,7 +122,8 @@ __device__ __forceinline__ void mutual_unit(const double4* __restrict__ sbuf, in
 struct Span {
   int q, off;  // stream position: task q (relative to A's first), particle off in it
   int n;       // particles in the unit
-  int64_t base;  // stream offset of the unit (partial slot - poff[t0])
+  int64_t base;  // stream offset of the unit (partial slot - poff[t0]); -1: A itself
+  bool dir;      // sources of directed tasks (another rank's leaves: A's sums only)
 };
 
 template <int NG, int TPL>
@@ -140,7 +142,7 @@ __device__ void mutual_leaf(const MutualArgs& m, int A, int lane, double4 (*buf)
     qi[k] = i < nA ? v.w : 0.0;
     fi[k] = 0.0;
   }
-  const int t0 = m.toff[A], nt = m.toff[A + 1] - t0;
+  const int t0 = m.toff[A], nt = m.toff[A + 1] - t0, nmt = m.tmend[A] - t0;
   // the first 32 tasks' source ranges, one per lane; later ones read when needed
   int my_b = 0, my_n = 0;
   if (lane < nt) {
@@ -156,8 +158,8 @@ __device__ void mutual_leaf(const MutualArgs& m, int A, int lane, double4 (*buf)
   int q = 0, off = 0;
   int64_t spos = 0;
   auto stage = [&](int bb) -> Span {
-    Span u{q, off, 0, spos};
-    while (q < nt && u.n < kU) {
+    Span u{q, off, 0, spos, q >= nmt};
+    while (q < nt && u.n < kU && (q < nmt) == !u.dir) {  // a unit never mixes mutual and directed
       int sb, nb;
       if (q < 32) {
         sb = __shfl_sync(0xffffffffu, my_b, q);
@@ -182,11 +184,11 @@ __device__ void mutual_leaf(const MutualArgs& m, int A, int lane, double4 (*buf)
   };
   copy(m.pos + ab, nA, buf[0]);  // unit 0: A itself
   mcp_commit();
-  Span cur{0, 0, nA, -1};
+  Span cur{0, 0, nA, -1, false};
   int bb = 0;
   while (true) {
     const bool more = q < nt;
-    Span nx{0, 0, 0, 0};
+    Span nx{0, 0, 0, 0, false};
     if (more) {
       nx = stage(bb ^ 1);
       mcp_wait<1>();
@@ -194,7 +196,7 @@ __device__ void mutual_leaf(const MutualArgs& m, int A, int lane, double4 (*buf)
       mcp_wait<0>();
     }
     __syncwarp();
-    if (cur.base < 0)
+    if (cur.base < 0 || cur.dir)  // A itself (r = 0 skipped), or directed sources
       self_unit<NS, TPL>(buf[bb], cur.n, b, xi, fi);
     else
       mutual_unit<NG, TPL>(buf[bb], cur.n, a, b, lane, xi, qi, fi, red, out0 + cur.base);
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(128) mutual_out_kernel(
     const int32_t* __restrict__ cend, const double4* __restrict__ center, const double4* __restrict__ pos,
     const double2* __restrict__ L, const double* __restrict__ own, const int32_t* __restrict__ goff,
     const int64_t* __restrict__ gslot, const double* __restrict__ partial, const uint32_t* __restrict__ perm,
-    double s_phi, double* __restrict__ phi_out) {
+    int64_t out_base, double s_phi, double* __restrict__ phi_out) {
   constexpr int NC = (P + 1) * (P + 2) / 2;
   __shared__ double2 Lsh[4][NC];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
@@ -306,14 +308,15 @@ __global__ void __launch_bounds__(128) mutual_out_kernel(
     double f = own[t];
     for (int g = g0; g < g1; ++g) f += partial[gslot[g] + (t - tb)];
     f += l2p_phi<P>(Lsh[wi], x.x - c.x, x.y - c.y, x.z - c.z);
-    phi_out[perm[t]] = f * s_phi;
+    phi_out[perm ? (int64_t)perm[t] : (int64_t)t - out_base] = f * s_phi;  // caller order, or owned order (LET)
   }
 }
 
 template <int P>
 void launch_mutual_out(const fmm_plan_s& Pl, const NearMutual& Mu, const int32_t* leaves, int64_t nl, double* phi) {
   mutual_out_kernel<P><<<cdiv(nl, 4), 128, 0, Pl.stream>>>(leaves, nl, Pl.cells.begin, Pl.cells.end, Pl.cells.center,
-                                                          Pl.pos, Pl.L, Mu.own, Mu.goff, Mu.gslot, Mu.partial, Pl.perm,
+                                                          Pl.pos, Pl.L, Mu.own, Mu.goff, Mu.gslot, Mu.partial,
+                                                          Pl.near_compact_out ? nullptr : Pl.perm.ptr, Pl.own_begin,
                                                           std::ldexp(1.0, -Pl.e), phi);
 }
 template <int... Ps>
@@ -325,96 +328,126 @@ void dispatch_mutual_out(int p, const fmm_plan_s& Pl, const NearMutual& Mu, cons
 }
 
 // setup, per entry k of the target-grouped P2P list (A = tgt[k], B = src[k]): the flags and sizes
-// the scans turn into the task lists, and the symmetry check — B's list must hold A exactly once
-// (that entry's index is kept for the reverse side: the task (B, A) when B < A).
+// the scans turn into the task lists. Only targets A this rank owns have tasks (one rank: all). For
+// an owned source B the pair is mutual — a task of A if B > A (with |B| partial slots), the reverse
+// side (B's task) if B < A — and B's list must hold A exactly once (that entry's index is kept for
+// the reverse side); a source owned by another rank is a directed task of A (A's sums only).
 __global__ void mutual_mark_kernel(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src,
                                    const int32_t* __restrict__ off, const int32_t* __restrict__ cb,
-                                   const int32_t* __restrict__ ce, int64_t np, int32_t* __restrict__ is_task,
+                                   const int32_t* __restrict__ ce, int64_t np, int64_t own_b, int64_t own_e,
+                                   int32_t* __restrict__ is_mt, int32_t* __restrict__ is_dt,
                                    int32_t* __restrict__ size, int32_t* __restrict__ is_rev,
                                    int32_t* __restrict__ rpos, int* __restrict__ bad) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= np) return;
   const int A = tgt[k], B = src[k];
-  int task = 0, sz = 0, rev = 0;
-  if (ce[A] - cb[A] > kMaxLeaf) atomicOr(bad, 1);
-  if (ce[A] - cb[A] > kSmallLeaf) atomicOr(bad, 4);  // (not a failure: the 16-group kernel)
-  if (B != A) {
-    int j = -1, cnt = 0;
-    for (int i = off[B]; i < off[B + 1]; ++i)
-      if (src[i] == A) {
-        j = i;
-        ++cnt;
+  int mt = 0, dt = 0, sz = 0, rev = 0;
+  const bool ownA = cb[A] >= own_b && ce[A] <= own_e, ownB = cb[B] >= own_b && ce[B] <= own_e;
+  if (ownA) {
+    if (ce[A] - cb[A] > kMaxLeaf) atomicOr(bad, 1);
+    if (ce[A] - cb[A] > kSmallLeaf) atomicOr(bad, 4);  // (not a failure: the 16-group kernel)
+    if (B != A && !ownB) {
+      dt = 1;
+    } else if (B != A) {
+      int j = -1, cnt = 0;
+      for (int i = off[B]; i < off[B + 1]; ++i)
+        if (src[i] == A) {
+          j = i;
+          ++cnt;
+        }
+      if (cnt != 1) atomicOr(bad, 2);
+      if (B > A) {
+        mt = 1;
+        sz = ce[B] - cb[B];
+      } else {
+        rev = 1;
+        rpos[k] = j;
       }
-    if (cnt != 1) atomicOr(bad, 2);
-    if (B > A) {
-      task = 1;
-      sz = ce[B] - cb[B];
-    } else {
-      rev = 1;
-      rpos[k] = j;
     }
   }
-  is_task[k] = task;
+  is_mt[k] = mt;
+  is_dt[k] = dt;
   size[k] = sz;
   is_rev[k] = rev;
 }
 
-// compaction: tasks (B, slot) in list order, the reverse side's slots in list order, and the
-// per-leaf offsets (a leaf's entries are off[A] .. off[A + 1]: the exclusive scans at off[A])
-__global__ void mutual_compact_kernel(const int32_t* __restrict__ src, int64_t np, const int32_t* __restrict__ is_task,
-                                      const int32_t* __restrict__ is_rev, const int32_t* __restrict__ rpos,
-                                      const int64_t* __restrict__ tscan, const int64_t* __restrict__ sscan,
-                                      const int64_t* __restrict__ rscan, int32_t* __restrict__ task_b,
+// compaction: per target A its mutual tasks (list order) then its directed tasks (list order); the
+// reverse side's slots in list order. Task index of a mutual entry: mutual tasks before it + directed
+// tasks of earlier targets; of a directed entry: mutual tasks up to A's last + directed before it.
+__global__ void mutual_compact_kernel(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src,
+                                      const int32_t* __restrict__ off, int64_t np, const int32_t* __restrict__ is_mt,
+                                      const int32_t* __restrict__ is_dt, const int32_t* __restrict__ is_rev,
+                                      const int32_t* __restrict__ rpos, const int64_t* __restrict__ mscan,
+                                      const int64_t* __restrict__ dscan, const int64_t* __restrict__ sscan,
+                                      const int64_t* __restrict__ rscan, int64_t nm, int32_t* __restrict__ task_b,
                                       int64_t* __restrict__ poff, int64_t* __restrict__ gslot) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= np) return;
-  if (is_task[k]) {
-    task_b[tscan[k]] = src[k];
-    poff[tscan[k]] = sscan[k];
+  const int A = tgt[k];
+  if (is_mt[k]) {
+    const int64_t t = mscan[k] + dscan[off[A]];
+    task_b[t] = src[k];
+    poff[t] = sscan[k];
+  } else if (is_dt[k]) {
+    const int64_t e = off[A + 1];
+    const int64_t t = (e < np ? mscan[e] : nm) + dscan[k];
+    task_b[t] = src[k];
+    poff[t] = 0;  // (unused: directed tasks have no partial slots)
   } else if (is_rev[k]) {
     gslot[rscan[k]] = sscan[rpos[k]];  // the slot of task (B, A) at its entry in B's list
   }
 }
 
 __global__ void mutual_offsets_kernel(const int32_t* __restrict__ off, int64_t nc, int64_t np,
-                                      const int64_t* __restrict__ tscan, const int64_t* __restrict__ rscan,
-                                      int64_t ntasks, int64_t nrev, int32_t* __restrict__ toff,
+                                      const int64_t* __restrict__ mscan, const int64_t* __restrict__ dscan,
+                                      const int64_t* __restrict__ rscan, int64_t nm, int64_t nd, int64_t nrev,
+                                      int32_t* __restrict__ toff, int32_t* __restrict__ tmend,
                                       int32_t* __restrict__ goff) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c > nc) return;
   const int64_t o = c < nc ? off[c] : np;
-  toff[c] = (int32_t)(o < np ? tscan[o] : ntasks);
+  const int64_t mo = o < np ? mscan[o] : nm, d = o < np ? dscan[o] : nd;
+  toff[c] = (int32_t)(mo + d);
   goff[c] = (int32_t)(o < np ? rscan[o] : nrev);
+  if (c < nc) {
+    const int64_t e = off[c + 1];
+    tmend[c] = (int32_t)((e < np ? mscan[e] : nm) + d);
+  }
 }
 
 }  // namespace
 
-// Task lists (setup, on the device): tasks (A, B > A) in A's list order with their partial slots,
-// and per leaf the slots of the tasks where it is the B side, in its list order. Disabled (the
-// directed path is kept) if the lists are not symmetric with each source at most once per list,
-// a leaf with pairs exceeds kMaxLeaf particles, or the partial buffer would take more than a
-// quarter of the free device memory.
+// Task lists (setup, on the device) for the targets this rank owns: mutual tasks (A, B > A) with
+// their partial slots, then directed tasks (sources owned by another rank), and per leaf the slots
+// of the tasks where it is the B side, in its list order. Disabled (the directed path is kept) if
+// the owned lists are not symmetric with each source at most once per list, a leaf with pairs
+// exceeds kMaxLeaf particles, or the partial buffer would take more than a quarter of the free
+// device memory.
 void near_mutual_setup(fmm_plan_s& P) {
   NearMutual& Mu = P.mutual;
   Mu.enabled = false;
-  if (P.world != 1 || P.dim != 3 || P.helmholtz || P.p2p.n == 0) return;
+  if (P.dim != 3 || P.helmholtz || P.p2p.n == 0) return;
   const int64_t nc = P.cells.n, np = P.p2p.n;
-  DevBuf<int32_t> is_task, size, is_rev, rpos;
-  DevBuf<int64_t> tscan, sscan, rscan;
+  DevBuf<int32_t> is_mt, is_dt, size, is_rev, rpos;
+  DevBuf<int64_t> mscan, dscan, sscan, rscan;
   DevBuf<int> bad;
-  is_task.alloc(np);
+  is_mt.alloc(np);
+  is_dt.alloc(np);
   size.alloc(np);
   is_rev.alloc(np);
   rpos.alloc(np);
-  tscan.alloc(np);
+  mscan.alloc(np);
+  dscan.alloc(np);
   sscan.alloc(np);
   rscan.alloc(np);
   bad.alloc(1);
   FMM_CUDA(cudaMemsetAsync(bad.ptr, 0, sizeof(int), P.stream));
   mutual_mark_kernel<<<cdiv(np, 256), 256, 0, P.stream>>>(P.p2p.tgt, P.p2p.src, P.p2p.off, P.cells.begin,
-                                                          P.cells.end, np, is_task, size, is_rev, rpos, bad);
+                                                          P.cells.end, np, P.own_begin, P.own_end, is_mt, is_dt, size,
+                                                          is_rev, rpos, bad);
   FMM_LAUNCHED("mutual_mark_kernel");
-  const int64_t ntasks = scan_counts_total(is_task, tscan, np, P.stream);
+  const int64_t nm = scan_counts_total(is_mt, mscan, np, P.stream);
+  const int64_t nd = scan_counts_total(is_dt, dscan, np, P.stream);
   const int64_t slots = scan_counts_total(size, sscan, np, P.stream);
   const int64_t nrev = scan_counts_total(is_rev, rscan, np, P.stream);
   int hbad = 0;
@@ -424,17 +457,20 @@ void near_mutual_setup(fmm_plan_s& P) {
   hbad &= 3;
   size_t mem_free = 0, mem_total = 0;
   FMM_CUDA(cudaMemGetInfo(&mem_free, &mem_total));
-  if (hbad || ntasks != nrev || (size_t)slots * 8 > mem_free / 4 || ntasks > INT32_MAX) return;
+  if (hbad || nm != nrev || (size_t)slots * 8 > mem_free / 4 || nm + nd > INT32_MAX) return;
+  const int64_t ntasks = nm + nd;
   Mu.toff.alloc(nc + 1);
+  Mu.tmend.alloc(std::max<int64_t>(1, nc));
   Mu.goff.alloc(nc + 1);
   Mu.task_b.alloc(std::max<int64_t>(1, ntasks));
   Mu.poff.alloc(std::max<int64_t>(1, ntasks));
   Mu.gslot.alloc(std::max<int64_t>(1, nrev));
-  mutual_compact_kernel<<<cdiv(np, 256), 256, 0, P.stream>>>(P.p2p.src, np, is_task, is_rev, rpos, tscan, sscan,
-                                                             rscan, Mu.task_b, Mu.poff, Mu.gslot);
+  mutual_compact_kernel<<<cdiv(np, 256), 256, 0, P.stream>>>(P.p2p.tgt, P.p2p.src, P.p2p.off, np, is_mt, is_dt, is_rev,
+                                                             rpos, mscan, dscan, sscan, rscan, nm, Mu.task_b, Mu.poff,
+                                                             Mu.gslot);
   FMM_LAUNCHED("mutual_compact_kernel");
-  mutual_offsets_kernel<<<cdiv(nc + 1, 256), 256, 0, P.stream>>>(P.p2p.off, nc, np, tscan, rscan, ntasks, nrev,
-                                                                  Mu.toff, Mu.goff);
+  mutual_offsets_kernel<<<cdiv(nc + 1, 256), 256, 0, P.stream>>>(P.p2p.off, nc, np, mscan, dscan, rscan, nm, nd, nrev,
+                                                                  Mu.toff, Mu.tmend, Mu.goff);
   FMM_LAUNCHED("mutual_offsets_kernel");
   Mu.partial.alloc(std::max<int64_t>(1, slots));
   Mu.own.alloc(std::max<int64_t>(1, P.n));
@@ -455,6 +491,7 @@ void near_mutual_pass(fmm_plan_s& P, double* phi) {
   m.cend = P.cells.end;
   m.pos = P.pos;
   m.toff = Mu.toff;
+  m.tmend = Mu.tmend;
   m.task_b = Mu.task_b;
   m.poff = Mu.poff;
   m.partial = Mu.partial;

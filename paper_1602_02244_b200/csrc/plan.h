@@ -122,13 +122,14 @@ struct NearMutual {
   bool enabled = false;
   bool big = false;  // a leaf with pairs has more than 64 particles (16 target groups x 2 source lanes)
   DevBuf<int32_t> toff, task_b;  // tasks (A, B > A) grouped by A: [ncells + 1], [ntasks]
+  DevBuf<int32_t> tmend;         // [ncells] end of A's mutual tasks (then directed: B on another rank)
   DevBuf<int64_t> poff;          // [ntasks] B-side partial slot
   DevBuf<int32_t> goff;          // [ncells + 1] per leaf, its B-side slots (gslot) in list order
   DevBuf<int64_t> gslot;
   DevBuf<double> partial, own;   // [sum of |B| over tasks], [n] (sorted order)
   int64_t ntasks = 0;
   int64_t bytes() const {
-    return toff.bytes() + task_b.bytes() + poff.bytes() + goff.bytes() + gslot.bytes() + partial.bytes() + own.bytes();
+    return toff.bytes() + tmend.bytes() + task_b.bytes() + poff.bytes() + goff.bytes() + gslot.bytes() + partial.bytes() + own.bytes();
   }
 };
 

@@ -291,6 +291,9 @@ def test_let_matvec_matches_single_gpu_and_oracle(dist_name, n, p, ncrit, theta,
     plans = [Plan(xd, p, ncrit, theta, rank=r, world=W) for r in range(W)]
     for pl in plans:
         pl.let_setup(list(counts))
+    # potentials: each rank evaluates the pairs of its own leaves once (mutual) and its halo pairs
+    # directed (csrc/near_mutual.cu); gradients take the directed near field
+    assert all(pl.stats()["near_mutual"] == 1 for pl in plans)
     res = let_matvec_local(plans, [qd[co[r]:co[r + 1]] for r in range(W)], grad=grad)
     single = Plan(xd, p, ncrit, theta).matvec(qd, grad=grad)
     torch.cuda.synchronize()

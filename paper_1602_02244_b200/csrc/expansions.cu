@@ -575,11 +575,8 @@ void upward_impl(fmm_plan_s& P, int64_t leaf_b, int64_t leaf_e, bool own = false
   }
   if (P.shift_variant == 1) {
     const size_t sh = sizeof(double2) * 24 * nc;
-    static size_t configured = 0;
-    if (sh > 48 * 1024 && sh > configured) {
+    if (sh > 48 * 1024)  // per call: the opt-in is per device context (no process-wide cache)
       FMM_CUDA(cudaFuncSetAttribute(m2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-      configured = sh;
-    }
     for (int l = P.max_level - 1; l >= 0; --l) {
       const LevelRange r = level_range(P, l, own);
       if (r.n <= 0) continue;

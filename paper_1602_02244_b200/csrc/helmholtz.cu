@@ -23,6 +23,7 @@
 #include <array>
 #include <map>
 #include <tuple>
+#include <mutex>
 #include <vector>
 
 #include "../../include/fmm_helmholtz.h"
@@ -39,12 +40,12 @@ __host__ __device__ inline int hidx(int n, int m) { return n * n + n + m; }
 
 // ------------------------------------------------------------------ host: special functions
 long double lfact(int n) {
-  static std::vector<long double> f;
-  if (f.empty()) {
-    f.resize(200);
-    f[0] = 1;
-    for (int i = 1; i < 200; ++i) f[i] = f[i - 1] * i;
-  }
+  static const std::vector<long double> f = [] {  // thread-safe one-time init
+    std::vector<long double> t(200);
+    t[0] = 1;
+    for (int i = 1; i < 200; ++i) t[i] = t[i - 1] * i;
+    return t;
+  }();
   return f[n];
 }
 
@@ -144,9 +145,10 @@ struct Coupling {
 };
 const Coupling& coupling(int p) {
   static Coupling C[kMaxPH + 1];
+  static std::mutex table_mu;  // plans may be set up from several host threads
+  std::lock_guard<std::mutex> lock(table_mu);
   Coupling& K = C[p];
   if (K.p == p) return K;
-  K.p = p;
   K.nc = (p + 1) * (p + 1);
   K.c.assign((size_t)K.nc * K.nc * (2 * p + 1), cld(0));
   const cld ipow[4] = {cld(1, 0), cld(0, 1), cld(-1, 0), cld(0, -1)};
@@ -163,6 +165,7 @@ const Coupling& coupling(int p) {
                 4 * kPiL * ipow[((n1 + l - n) % 4 + 4) % 4] * g;
           }
         }
+  K.p = p;  // complete
   return K;
 }
 

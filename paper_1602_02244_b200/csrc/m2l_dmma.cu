@@ -1009,9 +1009,7 @@ void m2l_dmma_pass(fmm_plan_s& P) {
   }
   const size_t sh = m2l_smem_bytes(D);
   const int threads = 32 * (D.nmt / 2);
-  static size_t configured[2] = {0, 0};  // dynamic-smem opt-in per kernel
   const int nmma = D.nmt / 2, nhelp = D.nhelp;
-  static size_t configured_ct[16] = {0};
   if (D.use_ws && P.p >= 5 && P.p <= 14 && getenv("FMM_M2L_NO_CT") == nullptr) {
     void (*k)(const M2LArgs, int) = nullptr;
     int thr = 0, nh = 0;
@@ -1027,19 +1025,15 @@ void m2l_dmma_pass(fmm_plan_s& P) {
       case 13: k = m2l_ws_ct_kernel<13>, thr = Geo<13>::THREADS, nh = Geo<13>::NHELP; break;
       default: k = m2l_ws_ct_kernel<14>, thr = Geo<14>::THREADS, nh = Geo<14>::NHELP; break;
     }
-    if (sh > 48 * 1024 && sh > configured_ct[P.p]) {
+    if (sh > 48 * 1024)  // per launch: the opt-in is per device context
       FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-      configured_ct[P.p] = sh;
-    }
     k<<<(unsigned)D.ntiles, thr, sh, P.stream>>>(a, nh);
     FMM_LAUNCHED("m2l_ws_ct_kernel");
     return;
   }
   if (D.use_ws) {
-    if (sh > 48 * 1024 && sh > configured[1]) {
+    if (sh > 48 * 1024)  // per launch: the opt-in is per device context
       FMM_CUDA(cudaFuncSetAttribute(m2l_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-      configured[1] = sh;
-    }
 #ifdef FMM_DEV  // development builds only: timing experiments (skips work: wrong results)
     const char* dbgs = getenv("FMM_M2L_DEBUG");
     const int dbg = dbgs ? atoi(dbgs) : 0;
@@ -1050,10 +1044,8 @@ void m2l_dmma_pass(fmm_plan_s& P) {
     FMM_LAUNCHED("m2l_ws_kernel");
     return;
   }
-  if (sh > 48 * 1024 && sh > configured[0]) {
+  if (sh > 48 * 1024)  // per launch: the opt-in is per device context
     FMM_CUDA(cudaFuncSetAttribute(m2l_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    configured[0] = sh;
-  }
   m2l_dmma_kernel<<<(unsigned)D.ntiles, threads, sh, P.stream>>>(a);
   FMM_LAUNCHED("m2l_dmma_kernel");
 }

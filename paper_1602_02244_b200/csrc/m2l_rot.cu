@@ -420,11 +420,8 @@ void m2l_rot_setup(fmm_plan_s& P) {
   int nent = 0;
   for (int n = 0; n <= p; ++n) nent += (n + 1) * (n + 1) + n * n;
   const size_t sh = sizeof(double2) * kQuadBatch * ncoef(p) + sizeof(double) * nent;
-  static size_t configured = 0;
-  if (sh > 48 * 1024 && sh > configured) {
+  if (sh > 48 * 1024)  // per call: the opt-in is per device context (no process-wide cache)
     FMM_CUDA(cudaFuncSetAttribute(build_rot_ops_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    configured = sh;
-  }
   build_rot_ops_kernel<<<(unsigned)D.nclass, kRotBuildThreads, sh, s>>>(D.class_keys, p, dgx, dgw, Rs, ditems, ni,
                                                                          blob, D.rot_ops);
   FMM_LAUNCHED("build_rot_ops_kernel");
@@ -531,12 +528,14 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
   const int dbg = 0;
 #endif
   r.prof = nullptr;
-  static DevBuf<unsigned long long> prof_buf;
-  if (dbg & 256) {  // timing experiment: per-warp cycle breakdown printed to stderr after the launch
-    if (!prof_buf.ptr) prof_buf.alloc(8 * 32);
+#ifdef FMM_DEV
+  DevBuf<unsigned long long> prof_buf;  // timing experiment: per-warp cycle breakdown printed to stderr
+  if (dbg & 256) {
+    prof_buf.alloc(8 * 32);
     FMM_CUDA(cudaMemsetAsync(prof_buf.ptr, 0, 8 * 32 * sizeof(unsigned long long), P.stream));
     r.prof = prof_buf.ptr;
   }
+#endif
   const size_t sh = rot_smem_bytes(P.p, a.T, D.rot_smax);
   // split small problems' tiles over several CTAs so that the grid covers the SMs (configs[1]: 73 tiles)
   // (one CTA per SM: minimise waves / split, ties to the smaller split; configs[1] -> 2, [2] -> 1)
@@ -565,11 +564,8 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
     if (D.rot_scratch.count < need) D.rot_scratch.alloc(need);
     r.scratch = D.rot_scratch.ptr;
   }
-  static size_t configured[17][2] = {};
-  if (sh > 48 * 1024 && sh > configured[P.p][split > 1]) {
+  if (sh > 48 * 1024)  // per launch: the opt-in is per device context (no process-wide cache)
     FMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    configured[P.p][split > 1] = sh;
-  }
   r.split = split;
   const dim3 grid((unsigned)(D.ntiles * split)), block(32 * (kRotMMA + rot_prep_warps(P.p) + rot_acc_warps(P.p) + kRotNear));
   k<<<grid, block, sh, P.stream>>>(r, dbg);
@@ -580,6 +576,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
                                                                   a.tile_cells, a.level, a.hpow, P.p, P.nc, a.L);
     FMM_LAUNCHED("rot_split_reduce_kernel");
   }
+#ifdef FMM_DEV
   if (dbg & 256) {
     unsigned long long h[8 * 32];
     FMM_CUDA(cudaMemcpyAsync(h, prof_buf.ptr, sizeof(h), cudaMemcpyDeviceToHost, P.stream));
@@ -589,6 +586,7 @@ void m2l_rot_launch(fmm_plan_s& P, const m2l::M2LArgs& a) {
               w, (double)h[8 * w] / h[8 * w + 5], (double)h[8 * w + 1] / h[8 * w + 5], (double)h[8 * w + 2] / h[8 * w + 5],
               (double)h[8 * w + 3] / h[8 * w + 5], (double)h[8 * w + 4] / h[8 * w + 5]);
   }
+#endif
 }
 
 }  // namespace fmm

@@ -846,12 +846,7 @@ void v4_switch(fmm_plan_s& P, const V4Args* a, int64_t npairs = 0) {
 bool m2l_v4_supported(int p) { return p >= kMinP && p <= kMaxP4; }
 
 void m2l_v4_setup(fmm_plan_s& P) {
-  static std::vector<double> table;  // host copy (same for every plan)
-  static bool built = false;
-  if (!built) {
-    table = build_f_table();
-    built = true;
-  }
+  static const std::vector<double> table = build_f_table();  // host copy, same for every plan (thread-safe init)
   FMM_CUDA(cudaMemcpyToSymbolAsync(fmm_c_F4, table.data(), sizeof(double) * kFTotal, 0, cudaMemcpyHostToDevice,
                                    P.stream));
   M2L4& V = P.m2l4;

@@ -637,7 +637,7 @@ fmm_status fmm_stats(fmm_plan P, fmm_stats_t* out) {
     b[FMM_B_TREE] = c.level.bytes() + c.begin.bytes() + c.end.bytes() + c.child.bytes() + c.nchild.bytes() +
                     c.parent.bytes() + c.anchor.bytes() + c.center.bytes() + P->leaves.bytes() + P->m2l4.ihalf.bytes();
     b[FMM_B_LISTS] = P->p2p.tgt.bytes() + P->p2p.src.bytes() + P->p2p.off.bytes() + P->m2l.tgt.bytes() +
-                     P->m2l.src.bytes() + P->m2l.off.bytes() + P->mutual.toff.bytes() + P->mutual.task_b.bytes() +
+                     P->m2l.src.bytes() + P->m2l.off.bytes() + P->mutual.toff.bytes() + P->mutual.tmend.bytes() + P->mutual.task_b.bytes() +
                      P->mutual.poff.bytes() + P->mutual.goff.bytes() + P->mutual.gslot.bytes();
     b[FMM_B_EXPANSIONS] = P->M.bytes() + P->L.bytes() + D.Mt.bytes() + P->m2l4.Mt.bytes() + P->helm.M.bytes() +
                           P->helm.L.bytes();

@@ -63,7 +63,10 @@ constexpr int kMinP = 2, kMaxP4 = 12;  // orders served by v4 (others: v3 / v2)
 constexpr int kUnitChunks = 4;         // chunks of 32 pairs per work unit (balanced at setup); 16 -> 4:
                                        // a CTA's warps on adjacent targets share source rows in L1
                                        // (configs[2] M2L 2.96 -> 2.78 ms, configs[3] 20.9 -> 19.8 ms)
-constexpr int kMaxWarpsPerCta = 8;     // M2L v4 CTA: up to 8 one-warp workers
+#ifndef FMM_V4_MAXW
+#define FMM_V4_MAXW 8  // register cap of the launch bounds: 8 -> 255 registers, 12 -> 168
+#endif
+constexpr int kMaxWarpsPerCta = FMM_V4_MAXW;  // M2L v4 CTA: up to this many one-warp workers
 
 
 __host__ __device__ constexpr int nnzF(int n) { return n * n + n + 1; }

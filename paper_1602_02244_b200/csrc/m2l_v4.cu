@@ -444,7 +444,13 @@ __device__ __forceinline__ void order_fence() { asm volatile("" ::: "memory"); }
 // blocks smaller than this many degrees are not fenced (the compiler may overlap them: more ILP
 // where one degree / order alone has little)
 #ifndef FMM_V4_STAGE_SYNC
-#define FMM_V4_STAGE_SYNC 1  // CTA barriers after stages 1 and 2 too (else once per chunk)
+#define FMM_V4_STAGE_SYNC 3  // CTA barriers between the stages: 0 none, 1 after stages 1 and 2, 2 after stage 1 only,
+                             // 3 after stage 2 only (with no chunk-end barrier; configs[2] M2L: 0 -> 3.85 ms, the warps
+                             // fetch the 112 KB of unrolled code apart; 1 2.64, 2 2.71, 3 2.64; configs[3] 20.7 / 18.3 / 18.4 / 18.1)
+#endif
+#ifndef FMM_V4_CHUNK_SYNC
+#define FMM_V4_CHUNK_SYNC 0  // CTA barrier at the end of every chunk too (configs[2] M2L 2.64 ms without, 2.79 with;
+                             // configs[3] 18.3 vs 19.8 ms: the warps' copy + segmented-sum imbalance waited on)
 #endif
 #ifndef FMM_V4_FENCE_MIN
 #define FMM_V4_FENCE_MIN 0
@@ -563,7 +569,7 @@ __device__ __noinline__ void pair_transform(double* w, double r, double2 e1, dou
   }
   const int z[4] = {0, 0, 0, 0};
   stage1_all<P>(w, r, 1.0, ca, cb, z);
-#if FMM_V4_STAGE_SYNC
+#if FMM_V4_STAGE_SYNC == 1 || FMM_V4_STAGE_SYNC == 2
   __syncthreads();
 #endif
   double h[2 * P + 1];  // Hankel entries k! / u^{k+1}
@@ -571,7 +577,7 @@ __device__ __noinline__ void pair_transform(double* w, double r, double2 e1, dou
 #pragma unroll
   for (int k = 1; k <= 2 * P; ++k) h[k] = h[k - 1] * (k * iu);
   stage2_all<P>(w, h);
-#if FMM_V4_STAGE_SYNC
+#if FMM_V4_STAGE_SYNC == 1 || FMM_V4_STAGE_SYNC == 3
   __syncthreads();
 #endif
   stage3_all<P>(w, ca, cb, z);
@@ -725,7 +731,11 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
           }
         }
       }
+#if FMM_V4_CHUNK_SYNC
       __syncthreads();
+#else
+      __syncwarp();
+#endif
     }
     if (cur >= 0) finish_segment<P>(a, u, cur, cur == tprev, cur == tnext, acc, lane);
   }

@@ -20,14 +20,27 @@ constexpr int kUnroll = FMM_NEAR_UNROLL;
 #ifndef FMM_NEAR_ORDER
 #define FMM_NEAR_ORDER 2
 #endif
+#ifndef FMM_NEAR_PF
+#define FMM_NEAR_PF 0  // interact(): the next source loaded an iteration ahead
+#endif
+#ifndef FMM_NEAR_XH
+#define FMM_NEAR_XH 0
+#endif
 __device__ __forceinline__ double rsqrt_fp64(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   if (FMM_NEAR_ORDER == 2) {  // one Newton step y + y (1 - x y^2) / 2, the halving of y done on
     // the exponent (integer pipe; y is a positive normal number): 3 FP64 ops instead of 4,
     // bitwise the same result (scaling by 2 commutes with rounding)
+#if FMM_NEAR_XH
+    // the same product from -x/2 (exponent and sign on x's high word, x's low word reused in
+    // place): (-x/2) y == -x (y/2) exactly, bitwise the same result, one register move less
+    const double xh = __hiloint2double(__double2hiint(x) + 0x7ff00000, __double2loint(x));
+    return fma(y, fma(xh * y, y, 0.5), y);
+#else
     const double yh = __hiloint2double(__double2hiint(y) - 0x00100000, __double2loint(y));
     return fma(y, fma(-x * yh, y, 0.5), y);
+#endif
   }
   const double e = fma(-x * y, y, 1.0);  // 1 - x y^2
   const double c = e * fma(e, 0.375, 0.5);  // e/2 + 3 e^2/8
@@ -37,9 +50,17 @@ __device__ __forceinline__ double rsqrt_fp64(double x) {
 template <bool kGrad, bool kCheck, int TPL>
 __device__ __forceinline__ void interact(const double4* __restrict__ sb, int ns, int sg, int G,
                                          const double3 (&xi)[TPL], double (&f)[TPL], double3 (&g)[TPL]) {
+#if FMM_NEAR_PF
+  double4 sn = sb[sg < ns ? sg : 0];  // the next source, loaded an iteration ahead
+#endif
 #pragma unroll kUnroll
   for (int j = sg; j < ns; j += G) {
+#if FMM_NEAR_PF
+    const double4 s = sn;
+    sn = sb[j + G < ns ? j + G : 0];
+#else
     const double4 s = sb[j];
+#endif
 #pragma unroll
     for (int k = 0; k < TPL; ++k) {
       const double dx = xi[k].x - s.x, dy = xi[k].y - s.y, dz = xi[k].z - s.z;

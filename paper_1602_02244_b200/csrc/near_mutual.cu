@@ -36,6 +36,9 @@ constexpr int kSmallLeaf = 64;  // up to here 8 target groups x 4 source lanes, 
 #ifndef FMM_MUTUAL_UNROLL
 #define FMM_MUTUAL_UNROLL 1  // source-loop unroll of the mutual units
 #endif
+#ifndef FMM_MUTUAL_PF
+#define FMM_MUTUAL_PF 1  // source loaded one loop iteration ahead (LDS latency off the chain; near 1.58 -> 1.53 ms at configs[2])
+#endif
 #ifndef FMM_MUTUAL_BUF
 #define FMM_MUTUAL_BUF 128
 #endif
@@ -74,8 +77,15 @@ struct MutualArgs {
 template <int NS, int TPL>
 __device__ __forceinline__ void self_unit(const double4* __restrict__ sbuf, int n, int b, const double3 (&xi)[TPL],
                                           double (&fi)[TPL]) {
+#if FMM_MUTUAL_PF
+  double4 sn = sbuf[b < n ? b : 0];
+  for (int j = b; j < n; j += NS) {
+    const double4 s = sn;
+    sn = sbuf[j + NS < n ? j + NS : 0];
+#else
   for (int j = b; j < n; j += NS) {
     const double4 s = sbuf[j];
+#endif
 #pragma unroll
     for (int k = 0; k < TPL; ++k) {
       const double dx = xi[k].x - s.x, dy = xi[k].y - s.y, dz = xi[k].z - s.z;
@@ -94,10 +104,18 @@ __device__ __forceinline__ void mutual_unit(const double4* __restrict__ sbuf, in
                                             const double3 (&xi)[TPL], const double (&qi)[TPL], double (&fi)[TPL],
                                             double* __restrict__ red, double* __restrict__ out) {
   constexpr int NS = 32 / NG;
+#if FMM_MUTUAL_PF
+  double4 sn = sbuf[b < n ? b : 0];  // the next source, loaded an iteration ahead
+#endif
 #pragma unroll kUnroll
   for (int j0 = 0; j0 < n; j0 += NS) {  // j < NS ceil(n / NS) <= kR
     const int j = j0 + b;
+#if FMM_MUTUAL_PF
+    double4 s = sn;
+    sn = sbuf[j + NS < n ? j + NS : 0];
+#else
     double4 s = sbuf[j < n ? j : 0];    // padding sources: source 0 with charge 0
+#endif
     if (j >= n) s.w = 0.0;
     double sb = 0.0;
 #pragma unroll

@@ -37,7 +37,8 @@ def _deps():
 
 
 def _flags_id() -> str:
-    return " ".join(NVFLAGS)
+    # (the checkout's own path left out: the same library is up to date wherever the tree is copied)
+    return " ".join(NVFLAGS).replace(ROOT, "$ROOT")
 
 
 def up_to_date() -> bool:

@@ -455,12 +455,49 @@ __device__ __forceinline__ void order_fence() { asm volatile("" ::: "memory"); }
 #ifndef FMM_V4_FENCE_MIN
 #define FMM_V4_FENCE_MIN 0
 #endif
+#ifndef FMM_V4_REFILL
+#define FMM_V4_REFILL 0  // rows refilled with the next chunk's sources inside the segmented sum (measured: configs[2]
+                         // M2L 2.63 -> 2.63 ms, configs[3] 18.1 -> 19.7 ms: the copy's latency was not the cost; kept off)
+#endif
+#ifndef FMM_V4_SKEW
+#define FMM_V4_SKEW 0  // k > 0 (with FMM_V4_STAGE_SYNC=0): the chunk's one CTA barrier is taken by warps 0-3 after degree
+                       // P - k of stage 1 and by the other warps at the end of stage 1, so the two warps of a scheduler
+                       // run k degree steps apart (one's shared-memory bursts under the other's FP64 bursts) while
+                       // both stay inside the instruction cache's window
+#endif
+#ifndef FMM_V4_GROUPS
+#define FMM_V4_GROUPS 1  // the CTA's warps in this many barrier groups (contiguous warps: one warp of each group per
+                         // scheduler), each in step on its own named barrier: one group's copy / segmented-sum
+                         // phases under another's FP64 phases, at the price of that many instruction streams
+#endif
+#ifndef FMM_V4_SKEW_NS
+#define FMM_V4_SKEW_NS 0  // group g starts g * this many ns late
+#endif
+
+// the stage barrier of the calling warp's group
+__device__ __forceinline__ void stage_barrier() {
+#if FMM_V4_GROUPS > 1
+  const int nw = blockDim.x >> 5, g = (int)(threadIdx.x >> 5) * FMM_V4_GROUPS / nw;
+  const int lo = (g * nw + FMM_V4_GROUPS - 1) / FMM_V4_GROUPS, hi = ((g + 1) * nw + FMM_V4_GROUPS - 1) / FMM_V4_GROUPS;
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(32 * (hi - lo)) : "memory");
+#else
+  __syncthreads();
+#endif
+}
 
 template <int P, int N = 0>
 __device__ __forceinline__ void stage1_all(double* w, double r, double rn, const double2* ca, const double2* cb,
                                            const int (&z)[4]) {
   stage1<N>(w, rn, ca, cb, z[0], z[1]);
   if constexpr (N >= FMM_V4_FENCE_MIN) order_fence();
+#if FMM_V4_SKEW
+  if constexpr (N == (P > FMM_V4_SKEW ? P - FMM_V4_SKEW : 0)) {
+    if (threadIdx.x < 128) asm volatile("bar.sync 0;" ::: "memory");
+  }
+  if constexpr (N == P) {
+    if (threadIdx.x >= 128) asm volatile("bar.sync 0;" ::: "memory");
+  }
+#endif
   if constexpr (N < P) stage1_all<P, N + 1>(w, r, rn * r, ca, cb, z);
 }
 template <int P, int M = 0>
@@ -471,6 +508,100 @@ __device__ __forceinline__ void stage2_all(double* w, const double* h) {
   if constexpr (P - M >= FMM_V4_FENCE_MIN) order_fence();
   if constexpr (M < P) stage2_all<P, M + 1>(w, h);
 }
+#ifndef FMM_V4_PIPE
+#define FMM_V4_PIPE 0  // software pipelining of the lane's shared-memory loads: the next step's inputs are loaded
+                       // before this step's FMAs (bit 0: stage 1, bit 1: stage 2, bit 2: stage 3); same arithmetic
+#endif
+#ifndef FMM_V4_PIPE_MAX
+#define FMM_V4_PIPE_MAX 8  // stages 1 / 3: highest degree whose inputs are loaded a step ahead (registers)
+#endif
+
+// stage 2 with the next (order, part)'s column loaded a step ahead
+template <int P, int M, int PART>
+__device__ __forceinline__ void stage2_pipe(double* w, const double* h, const double (&a)[P + 1 - M]) {
+  constexpr int L = P + 1 - M;
+  constexpr bool last = M == P && (PART == 1 || M == 0);
+  constexpr int MN = (PART == 0 && M > 0) ? M : M + 1, PN = (PART == 0 && M > 0) ? 1 : 0;
+  double an[last ? 1 : P + 1 - MN];
+  if constexpr (!last) {
+#pragma unroll
+    for (int i = 0; i < P + 1 - MN; ++i) an[i] = w[(MN + i) * (MN + i) + ridx(MN, PN)];
+  }
+  double y[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int n = 0; n < L; ++n) s = fma(h[2 * M + j + n], a[n], s);
+    y[j] = M == 0 ? 0.5 * s : s;
+  }
+#pragma unroll
+  for (int i = 0; i < L; ++i) w[(M + i) * (M + i) + ridx(M, PART)] = y[i];
+  order_fence();
+  if constexpr (!last) stage2_pipe<P, MN, PN>(w, h, an);
+}
+template <int P>
+__device__ __forceinline__ void stage2_piped(double* w, const double* h) {
+  double a0[P + 1];
+#pragma unroll
+  for (int i = 0; i < P + 1; ++i) a0[i] = w[i * i];
+  stage2_pipe<P, 0, 0>(w, h, a0);
+}
+
+// stages 1 / 3 with the next degree's inputs loaded a step ahead (degrees <= FMM_V4_PIPE_MAX)
+template <int P, int N>
+__device__ __forceinline__ void stage1_pipe(double* w, double r, double rn, const double2* ca, const double2* cb,
+                                            const int (&z)[4], const double (&xin)[2 * N + 1]) {
+  constexpr bool pre = N < P && N + 1 <= FMM_V4_PIPE_MAX;
+  double xn[N < P ? 2 * N + 3 : 1];
+  if constexpr (pre) {
+#pragma unroll
+    for (int i = 0; i < 2 * N + 3; ++i) xn[i] = w[(N + 1) * (N + 1) + i];
+  }
+  double x[2 * N + 1], t[2 * N + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) x[i] = xin[i] * rn;
+  zrot<N>(x, ca);
+  apply_fixed<N, false, true, false>(x, t, z[0]);
+  zrot<N>(t, cb);
+  apply_fixed<N, false, false, false>(t, x, z[1]);
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) w[N * N + i] = x[i];
+  order_fence();
+  if constexpr (N < P) {
+    if constexpr (!pre) {
+#pragma unroll
+      for (int i = 0; i < 2 * N + 3; ++i) xn[i] = w[(N + 1) * (N + 1) + i];
+    }
+    stage1_pipe<P, N + 1>(w, r, rn * r, ca, cb, z, xn);
+  }
+}
+template <int P, int N>
+__device__ __forceinline__ void stage3_pipe(double* w, const double2* ca, const double2* cb, const int (&z)[4],
+                                            const double (&xin)[2 * N + 1]) {
+  constexpr bool pre = N < P && N + 1 <= FMM_V4_PIPE_MAX;
+  double xn[N < P ? 2 * N + 3 : 1];
+  if constexpr (pre) {
+#pragma unroll
+    for (int i = 0; i < 2 * N + 3; ++i) xn[i] = w[(N + 1) * (N + 1) + i];
+  }
+  double x[2 * N + 1], t[2 * N + 1];
+  apply_fixed<N, true, true, true>(xin, t, z[2]);
+  zrot<N>(t, cb);
+  apply_fixed<N, true, false, false>(t, x, z[3]);
+  zrot<N>(x, ca);
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) w[N * N + i] = x[i];
+  order_fence();
+  if constexpr (N < P) {
+    if constexpr (!pre) {
+#pragma unroll
+      for (int i = 0; i < 2 * N + 3; ++i) xn[i] = w[(N + 1) * (N + 1) + i];
+    }
+    stage3_pipe<P, N + 1>(w, ca, cb, z, xn);
+  }
+}
+
 template <int P, int N = 0>
 __device__ __forceinline__ void stage3_all(double* w, const double2* ca, const double2* cb, const int (&z)[4]) {
   stage3<N>(w, ca, cb, z[2], z[3]);
@@ -568,19 +699,37 @@ __device__ __noinline__ void pair_transform(double* w, double r, double2 e1, dou
     cb[m] = make_double2(fma(cb[m - 1].x, e2.x, -cb[m - 1].y * e2.y), fma(cb[m - 1].x, e2.y, cb[m - 1].y * e2.x));
   }
   const int z[4] = {0, 0, 0, 0};
+#if FMM_V4_PIPE & 1
+  {
+    const double x0[1] = {w[0]};
+    stage1_pipe<P, 0>(w, r, 1.0, ca, cb, z, x0);
+  }
+#else
   stage1_all<P>(w, r, 1.0, ca, cb, z);
+#endif
 #if FMM_V4_STAGE_SYNC == 1 || FMM_V4_STAGE_SYNC == 2
-  __syncthreads();
+  stage_barrier();
 #endif
   double h[2 * P + 1];  // Hankel entries k! / u^{k+1}
   h[0] = iu;
 #pragma unroll
   for (int k = 1; k <= 2 * P; ++k) h[k] = h[k - 1] * (k * iu);
+#if FMM_V4_PIPE & 2
+  stage2_piped<P>(w, h);
+#else
   stage2_all<P>(w, h);
-#if FMM_V4_STAGE_SYNC == 1 || FMM_V4_STAGE_SYNC == 3
-  __syncthreads();
 #endif
+#if FMM_V4_STAGE_SYNC == 1 || FMM_V4_STAGE_SYNC == 3
+  stage_barrier();
+#endif
+#if FMM_V4_PIPE & 4
+  {
+    const double x0[1] = {w[0]};
+    stage3_pipe<P, 0>(w, ca, cb, z, x0);
+  }
+#else
   stage3_all<P>(w, ca, cb, z);
+#endif
 }
 #endif
 
@@ -597,7 +746,39 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
   // units and chunks (a barrier after each stage keeps the warps on the same instructions:
   // the unrolled code is larger than the instruction cache, so warps in step share its fetches)
   const int64_t per_round = (int64_t)gridDim.x * nw;
+#if FMM_V4_GROUPS > 1 && FMM_V4_SKEW_NS > 0
+  for (int k = warp * FMM_V4_GROUPS / nw; k > 0; --k) __nanosleep(FMM_V4_SKEW_NS);
+#endif
   const int rounds = (int)((a.nunits + per_round - 1) / per_round);
+#if FMM_V4_REFILL
+  // FMM_V4_REFILL: a row of the warp's buffer is refilled with the NEXT chunk's source row (of this unit or of
+  // the warp's next unit) as soon as the segmented sum has read it, so the copies' issue and L2 latency run
+  // under the sum and the next chunk's geometry instead of after them (same sums in the same order).
+  auto chunk_range = [&](int it, int ich, int64_t& base, int& nact) {
+    const int64_t u = ((int64_t)it * gridDim.x + blockIdx.x) * nw + warp;
+    const int64_t u0 = min(u * UP, a.npairs), u1 = min(u0 + UP, a.npairs);
+    base = u0 + 32 * ich;
+    nact = (int)max((int64_t)0, min((int64_t)32, u1 - base));
+  };
+  int64_t base_n = 0;
+  int nact_n = 0, tg_next = -1, sr_next = 0;
+  auto copy_row = [&](int l) {  // row l of the next chunk (l warp-uniform, < nact_n)
+    const int s = __shfl_sync(0xffffffffu, sr_next, l);
+    const double* g = a.Mt + (int64_t)s * NR;
+#pragma unroll
+    for (int c = 0; c < KPL; ++c) {
+      const int q = lane + 32 * c;
+      if (q < NR) cp_async8(wb + l * NRS + q, g + q);
+    }
+  };
+  if (rounds > 0) {
+    chunk_range(0, 0, base_n, nact_n);
+    tg_next = lane < nact_n ? a.tgt[base_n + lane] : -1;
+    sr_next = lane < nact_n ? a.src[base_n + lane] : 0;
+#pragma unroll 8
+    for (int l = 0; l < nact_n; ++l) copy_row(l);
+  }
+#endif
   for (int it = 0; it < rounds; ++it) {
     const int64_t u = ((int64_t)it * gridDim.x + blockIdx.x) * nw + warp;  // may be >= nunits: idle
     const int64_t u0 = min(u * UP, a.npairs), u1 = min(u0 + UP, a.npairs);
@@ -607,9 +788,24 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
     double acc[KPL];
 #pragma unroll
     for (int c = 0; c < KPL; ++c) acc[c] = 0.0;
+#if !FMM_V4_REFILL
     // the chunk's (target, source) pairs, loaded one chunk ahead (their latency off the critical path)
     int tg_next = lane < u1 - u0 ? a.tgt[u0 + lane] : -1, sr_next = lane < u1 - u0 ? a.src[u0 + lane] : 0;
+#endif
     for (int ich = 0; ich < a.uchunks; ++ich) {
+#if FMM_V4_REFILL
+      const int nact = nact_n;
+      const bool act = lane < nact;
+      const int tg = tg_next, sr = sr_next;
+      if (it + 1 < rounds || ich + 1 < a.uchunks) {
+        const bool same = ich + 1 < a.uchunks;
+        chunk_range(same ? it : it + 1, same ? ich + 1 : 0, base_n, nact_n);
+      } else {
+        nact_n = 0;
+      }
+      tg_next = lane < nact_n ? a.tgt[base_n + lane] : -1;
+      sr_next = lane < nact_n ? a.src[base_n + lane] : 0;
+#else
       const int64_t base = u0 + 32 * ich;
       const int nact = (int)max((int64_t)0, min((int64_t)32, u1 - base));
       const bool act = lane < nact;
@@ -630,6 +826,7 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
           if (q < NR) cp_async8(wb + l * NRS + q, g + q);
         }
       }
+#endif
       // geometry of the lane's pair (overlaps the copies)
       // (inactive lanes of a ragged chunk run the same code on the chunk's first pair and their
       // own stale rows — no divergence, results unused: the stages stay warp-uniform)
@@ -714,6 +911,30 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
 #pragma unroll
             for (int c = 0; c < KPL; ++c) acc[c] = 0.0;
           }
+#if FMM_V4_REFILL
+          double ps[KPL][4];
+#pragma unroll
+          for (int c = 0; c < KPL; ++c) ps[c][0] = ps[c][1] = ps[c][2] = ps[c][3] = 0.0;
+          int l = s0;
+          for (; l + 3 < s1; l += 4) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int c = 0; c < KPL; ++c)
+                if (lane + 32 * c < NR) ps[c][j] += wb[(l + j) * NRS + lane + 32 * c];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (l + j < nact_n) copy_row(l + j);
+          }
+          for (; l < s1; ++l) {
+#pragma unroll
+            for (int c = 0; c < KPL; ++c)
+              if (lane + 32 * c < NR) ps[c][0] += wb[l * NRS + lane + 32 * c];
+            if (l < nact_n) copy_row(l);
+          }
+#pragma unroll
+          for (int c = 0; c < KPL; ++c) acc[c] += (ps[c][0] + ps[c][1]) + (ps[c][2] + ps[c][3]);
+#else
 #pragma unroll
           for (int c = 0; c < KPL; ++c) {
             const int k = lane + 32 * c;
@@ -729,7 +950,11 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
             for (; l < s1; ++l) p0 += wb[l * NRS + k];
             acc[c] += (p0 + p1) + (p2 + p3);
           }
+#endif
         }
+#if FMM_V4_REFILL
+        for (int l = nact; l < nact_n; ++l) copy_row(l);  // rows the finished chunk did not use
+#endif
       }
 #if FMM_V4_CHUNK_SYNC
       __syncthreads();

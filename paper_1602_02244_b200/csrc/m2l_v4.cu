@@ -662,6 +662,9 @@ __device__ __forceinline__ void write_target(const V4Args& a, int t, const doubl
     while ((j + 1) * (j + 1) <= q) ++j;
     const int r = q - j * j, m = (r + 1) >> 1, part = r > 0 ? ((r + 1) & 1) : 0;
     double s = m == 0 ? 2.0 * ih : ih;
+#if FMM_V4_REP
+    if (m & 1) s = -s;  // the deferred S = diag((-1)^m) of stage 3
+#endif
     for (int k = 0; k < j; ++k) s *= ih;
     Lc[2 * cidx(j, m) + part] = acc[c] * s;
   }
@@ -683,7 +686,120 @@ __device__ __forceinline__ void finish_segment(const V4Args& a, int64_t u, int t
     if (lane + 32 * c < NR) d[lane + 32 * c] = acc[c];
 }
 
-#if FMM_V4_CIMM
+#ifndef FMM_V4_REP
+#define FMM_V4_REP 0  // one code body for both fixed-operator applications of a stage, run twice over the row:
+                      // G = S F S with S = diag((-1)^m) = the z-rotation by pi, folded into the angles, so
+                      //   stage 1 = T(b + pi) T(a + pi),           T(t) = F zrot(t)
+                      //   stage 3 = S U(a + pi) U(b + pi) K,       U(t) = zrot(t) F^T, K = conjugation (the sign of
+                      // stage 2's Im outputs), S applied once per target in write_target; r^n moves to stage 2's
+                      // input. 31 % fewer unique instructions per pair for two more passes over the row in shared
+                      // memory; parity-tested, measured slower (configs[2] M2L 2.62 -> 3.14 ms, configs[3] 18.1 ->
+                      // 20.8 ms: the added shared-memory wavefronts cost their full time, profiles/r2_m2l_bound.md); off.
+#endif
+#if FMM_V4_REP
+template <int N>
+__device__ __forceinline__ void body1(double* w, const double2* cs) {
+  double x[2 * N + 1], t[2 * N + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) x[i] = w[N * N + i];
+  zrot<N>(x, cs);
+  apply_fixed<N, false, false, false>(x, t, 0);
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) w[N * N + i] = t[i];
+}
+template <int N>
+__device__ __forceinline__ void body3(double* w, const double2* cs) {
+  double x[2 * N + 1], t[2 * N + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) x[i] = w[N * N + i];
+  apply_fixed<N, true, false, false>(x, t, 0);
+  zrot<N>(t, cs);
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) w[N * N + i] = t[i];
+}
+template <int P, int N = 0>
+__device__ __forceinline__ void body1_all(double* w, const double2* cs) {
+  body1<N>(w, cs);
+  order_fence();
+  if constexpr (N < P) body1_all<P, N + 1>(w, cs);
+}
+template <int P, int N = 0>
+__device__ __forceinline__ void body3_all(double* w, const double2* cs) {
+  body3<N>(w, cs);
+  order_fence();
+  if constexpr (N < P) body3_all<P, N + 1>(w, cs);
+}
+// stage 2 with the source scaling r^n on its input and conjugated (negated Im) output
+template <int P, int M, int PART>
+__device__ __forceinline__ void stage2r(double* w, const double* h, const double* rp) {
+  constexpr int L = P + 1 - M;
+  double a[L], y[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) a[i] = w[(M + i) * (M + i) + ridx(M, PART)] * rp[M + i];
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int n = 0; n < L; ++n) s = PART ? fma(-h[2 * M + j + n], a[n], s) : fma(h[2 * M + j + n], a[n], s);
+    y[j] = M == 0 ? 0.5 * s : s;
+  }
+#pragma unroll
+  for (int i = 0; i < L; ++i) w[(M + i) * (M + i) + ridx(M, PART)] = y[i];
+}
+template <int P, int M = 0>
+__device__ __forceinline__ void stage2r_all(double* w, const double* h, const double* rp) {
+  stage2r<P, M, 0>(w, h, rp);
+  order_fence();
+  if constexpr (M > 0) stage2r<P, M, 1>(w, h, rp);
+  order_fence();
+  if constexpr (M < P) stage2r_all<P, M + 1>(w, h, rp);
+}
+template <int P>
+__device__ __forceinline__ void phasors(double2 (&cs)[P + 1], double2 e) {
+  cs[0] = make_double2(1.0, 0.0);
+  cs[1] = e;
+#pragma unroll
+  for (int m = 2; m <= P; ++m)
+    cs[m] = make_double2(fma(cs[m - 1].x, e.x, -cs[m - 1].y * e.y), fma(cs[m - 1].x, e.y, cs[m - 1].y * e.x));
+}
+// one pass of a stage over the row: called twice (two call sites, one copy of the code; not a loop — inside
+// a loop the compiler would hoist the fixed operator's constants into registers and spill them)
+template <int P>
+__device__ __noinline__ void pass1(double* w, double2 e) {
+  double2 cs[P + 1];
+  phasors<P>(cs, e);
+  body1_all<P>(w, cs);
+}
+template <int P>
+__device__ __noinline__ void pass3(double* w, double2 e) {
+  double2 cs[P + 1];
+  phasors<P>(cs, e);
+  body3_all<P>(w, cs);
+}
+template <int P>
+__device__ __noinline__ void pass2(double* w, double r, double iu) {
+  double h[2 * P + 1], rp[P + 1];  // Hankel entries k! / u^{k+1}; r^n
+  h[0] = iu;
+#pragma unroll
+  for (int k = 1; k <= 2 * P; ++k) h[k] = h[k - 1] * (k * iu);
+  rp[0] = 1.0;
+#pragma unroll
+  for (int n = 1; n <= P; ++n) rp[n] = rp[n - 1] * r;
+  stage2r_all<P>(w, h, rp);
+}
+template <int P>
+__device__ __forceinline__ void pair_transform(double* w, double r, double2 e1, double2 e2, double iu) {
+  const double2 ea = make_double2(-e1.x, -e1.y), eb = make_double2(-e2.x, -e2.y);  // angles a + pi, b + pi
+  pass1<P>(w, ea);
+  pass1<P>(w, eb);
+  pass2<P>(w, r, iu);
+#if FMM_V4_STAGE_SYNC == 1 || FMM_V4_STAGE_SYNC == 3
+  stage_barrier();
+#endif
+  pass3<P>(w, eb);
+  pass3<P>(w, ea);
+}
+#elif FMM_V4_CIMM
 // one pair's rotation-translation-rotation, in place in the lane's row w. Not inlined: the fixed
 // operator's constant-bank entries are then DFMA operands at immediate addresses (no load
 // instruction) that the compiler cannot hoist out of the chunk loop into registers.

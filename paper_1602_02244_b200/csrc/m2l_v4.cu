@@ -455,6 +455,11 @@ __device__ __forceinline__ void order_fence() { asm volatile("" ::: "memory"); }
 #ifndef FMM_V4_FENCE_MIN
 #define FMM_V4_FENCE_MIN 0
 #endif
+#ifndef FMM_V4_COPY_ALIGNED
+#define FMM_V4_COPY_ALIGNED 0  // cp.async instructions on 256-byte-aligned shared-memory windows (5 per row instead of
+                                // 4): measured slower (configs[2] M2L 2.63 -> 2.71 ms); the copy's 480 wavefronts per
+                                // chunk (242 ideal) are not a line-alignment effect
+#endif
 #ifndef FMM_V4_REFILL
 #define FMM_V4_REFILL 0  // rows refilled with the next chunk's sources inside the segmented sum (measured: configs[2]
                          // M2L 2.63 -> 2.63 ms, configs[3] 18.1 -> 19.7 ms: the copy's latency was not the cost; kept off)
@@ -647,6 +652,23 @@ struct V4Geo {
   static constexpr int KPL = (NR + 31) / 32;
 };
 
+#ifndef FMM_V4_REP
+#define FMM_V4_REP 0  // one code body for both fixed-operator applications of a stage, run twice over the row:
+                      // G = S F S with S = diag((-1)^m) = the z-rotation by pi, folded into the angles, so
+                      //   stage 1 = T(b + pi) T(a + pi),           T(t) = F zrot(t)
+                      //   stage 3 = S U(a + pi) U(b + pi) K,       U(t) = zrot(t) F^T, K = conjugation (the sign of
+                      // stage 2's Im outputs), S applied once per target in write_target; r^n moves to stage 2's
+                      // input. 31 % fewer unique instructions per pair for two more passes over the row in shared
+                      // memory; parity-tested, measured slower (configs[2] M2L 2.62 -> 3.14 ms, configs[3] 18.1 ->
+                      // 20.8 ms: the added shared-memory wavefronts cost their full time, profiles/r2_m2l_bound.md); off.
+#endif
+#ifndef FMM_V4_REP_MINP
+#define FMM_V4_REP_MINP 11  // orders from this one up use the shared-body form: at p = 12 the pair function is 140 KB and
+                            // the kernel waits on instructions (no_instruction 2.9 warps per issue, FP64 pipe 24 %):
+                            // configs[4] M2L 227 -> 216 ms
+#endif
+template <int P>
+constexpr bool use_rep = FMM_V4_REP != 0 || P >= FMM_V4_REP_MINP;
 // Lambda = V Lambda~ / h^{j+1} (V: m = 0 entries x 2) of target t from the per-lane sums (lane k
 // owns real coefficients q = k + 32 c), into the complex (n, m >= 0) layout of L
 template <int P>
@@ -662,9 +684,9 @@ __device__ __forceinline__ void write_target(const V4Args& a, int t, const doubl
     while ((j + 1) * (j + 1) <= q) ++j;
     const int r = q - j * j, m = (r + 1) >> 1, part = r > 0 ? ((r + 1) & 1) : 0;
     double s = m == 0 ? 2.0 * ih : ih;
-#if FMM_V4_REP
-    if (m & 1) s = -s;  // the deferred S = diag((-1)^m) of stage 3
-#endif
+    if constexpr (use_rep<P>) {
+      if (m & 1) s = -s;  // the deferred S = diag((-1)^m) of stage 3 (shared-body form)
+    }
     for (int k = 0; k < j; ++k) s *= ih;
     Lc[2 * cidx(j, m) + part] = acc[c] * s;
   }
@@ -686,17 +708,6 @@ __device__ __forceinline__ void finish_segment(const V4Args& a, int64_t u, int t
     if (lane + 32 * c < NR) d[lane + 32 * c] = acc[c];
 }
 
-#ifndef FMM_V4_REP
-#define FMM_V4_REP 0  // one code body for both fixed-operator applications of a stage, run twice over the row:
-                      // G = S F S with S = diag((-1)^m) = the z-rotation by pi, folded into the angles, so
-                      //   stage 1 = T(b + pi) T(a + pi),           T(t) = F zrot(t)
-                      //   stage 3 = S U(a + pi) U(b + pi) K,       U(t) = zrot(t) F^T, K = conjugation (the sign of
-                      // stage 2's Im outputs), S applied once per target in write_target; r^n moves to stage 2's
-                      // input. 31 % fewer unique instructions per pair for two more passes over the row in shared
-                      // memory; parity-tested, measured slower (configs[2] M2L 2.62 -> 3.14 ms, configs[3] 18.1 ->
-                      // 20.8 ms: the added shared-memory wavefronts cost their full time, profiles/r2_m2l_bound.md); off.
-#endif
-#if FMM_V4_REP
 template <int N>
 __device__ __forceinline__ void body1(double* w, const double2* cs) {
   double x[2 * N + 1], t[2 * N + 1];
@@ -788,7 +799,7 @@ __device__ __noinline__ void pass2(double* w, double r, double iu) {
   stage2r_all<P>(w, h, rp);
 }
 template <int P>
-__device__ __forceinline__ void pair_transform(double* w, double r, double2 e1, double2 e2, double iu) {
+__device__ __forceinline__ void pair_transform_rep(double* w, double r, double2 e1, double2 e2, double iu) {
   const double2 ea = make_double2(-e1.x, -e1.y), eb = make_double2(-e2.x, -e2.y);  // angles a + pi, b + pi
   pass1<P>(w, ea);
   pass1<P>(w, eb);
@@ -799,7 +810,7 @@ __device__ __forceinline__ void pair_transform(double* w, double r, double2 e1, 
   pass3<P>(w, eb);
   pass3<P>(w, ea);
 }
-#elif FMM_V4_CIMM
+#if FMM_V4_CIMM
 // one pair's rotation-translation-rotation, in place in the lane's row w. Not inlined: the fixed
 // operator's constant-bank entries are then DFMA operands at immediate addresses (no load
 // instruction) that the compiler cannot hoist out of the chunk loop into registers.
@@ -854,7 +865,7 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
   using G = V4Geo<P>;
   constexpr int NR = G::NR, NRS = G::NRS, KPL = G::KPL;
   const int64_t UP = 32 * (int64_t)a.uchunks;
-  extern __shared__ double sm4[];
+  extern __shared__ __align__(256) double sm4[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double* const wb = sm4 + (size_t)warp * 32 * NRS;
   double* const w = wb + lane * NRS;
@@ -932,6 +943,22 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
         sr_next = nb < u1 ? a.src[nb] : 0;
       }
       // 1. source rows into the lanes' buffers (coalesced: row by row)
+#if FMM_V4_COPY_ALIGNED
+      // every cp.async instruction writes one 256-byte-aligned window of shared memory (two wavefronts):
+      // the rows start at odd 8-byte offsets, so a row is KPL + 1 windows with the ends masked
+#pragma unroll 8
+      for (int l = 0; l < nact; ++l) {
+        const int s = __shfl_sync(0xffffffffu, sr, l);
+        const int off = l * NRS, q0 = lane - (off & 31);  // the lane's coefficient in the row's first window
+        const double* g = a.Mt + (int64_t)s * NR;
+        double* d = wb + off;
+#pragma unroll
+        for (int c = 0; c <= KPL; ++c) {
+          const int q = q0 + 32 * c;
+          if (q >= 0 && q < NR) cp_async8(d + q, g + q);
+        }
+      }
+#else
 #pragma unroll 8
       for (int l = 0; l < nact; ++l) {
         const int s = __shfl_sync(0xffffffffu, sr, l);
@@ -942,6 +969,7 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
           if (q < NR) cp_async8(wb + l * NRS + q, g + q);
         }
       }
+#endif
 #endif
       // geometry of the lane's pair (overlaps the copies)
       // (inactive lanes of a ragged chunk run the same code on the chunk's first pair and their
@@ -974,7 +1002,10 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
 #if FMM_V4_CIMM
       cp_async_wait_all();
       __syncwarp();
-      pair_transform<P>(w, r, e1, e2, iu);
+      if constexpr (use_rep<P>)
+        pair_transform_rep<P>(w, r, e1, e2, iu);
+      else
+        pair_transform<P>(w, r, e1, e2, iu);
 #else
       ca[0] = cb[0] = make_double2(1.0, 0.0);
       ca[1] = e1;

@@ -810,6 +810,129 @@ __device__ __forceinline__ void pair_transform_rep(double* w, double r, double2 
   pass3<P>(w, eb);
   pass3<P>(w, ea);
 }
+#ifndef FMM_V4_TMEM
+#define FMM_V4_TMEM 0  // the lane-private hand-offs stage 1 -> 2 -> 3 through tensor memory (32x32b tcgen05.st / ld:
+                       // thread i <-> TMEM lane i, the row as 2 NR 32-bit columns) instead of shared memory:
+                       // 4 of the 8 passes over the row leave the shared-memory pipe (orders p <= 10, <= 8 warps)
+#endif
+template <int P>
+constexpr bool use_tmem = FMM_V4_TMEM != 0 && P <= 10 && !use_rep<P>;
+__shared__ uint32_t tm_base_s;  // the CTA's tensor-memory allocation (written by tcgen05.alloc)
+// the calling warp's region, from warp-uniform values only (a uniform-register address for LDTM / STTM)
+__device__ __forceinline__ uint32_t tm_warp_base() {
+  const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+  return tm_base_s + ((warp & 3u) << 21) + (warp >> 2) * 256u;
+}
+
+__device__ __forceinline__ void tm_st(uint32_t addr, double v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(__double2loint(v)),
+               "r"(__double2hiint(v))
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld(uint32_t addr, int& lo, int& hi) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// the loaded halves are defined only after tm_wait_ld: this keeps their uses behind it
+__device__ __forceinline__ double tm_value(int lo, int hi) {
+  asm volatile("" : "+r"(lo), "+r"(hi));
+  return __hiloint2double(hi, lo);
+}
+
+template <int N>
+__device__ __forceinline__ void stage1_t(const double* w, uint32_t tm, double rn, const double2* ca, const double2* cb) {
+  double x[2 * N + 1], t[2 * N + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) x[i] = w[N * N + i] * rn;
+  zrot<N>(x, ca);
+  apply_fixed<N, false, true, false>(x, t, 0);
+  zrot<N>(t, cb);
+  apply_fixed<N, false, false, false>(t, x, 0);
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) tm_st(tm + 2 * (N * N + i), x[i]);
+}
+template <int P, int M, int PART>
+__device__ __forceinline__ void stage2_t(uint32_t tm, const double* h) {
+  constexpr int L = P + 1 - M;
+  int lo[L], hi[L];
+  double a[L], y[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) tm_ld(tm + 2 * ((M + i) * (M + i) + ridx(M, PART)), lo[i], hi[i]);
+  tm_wait_ld();
+#pragma unroll
+  for (int i = 0; i < L; ++i) a[i] = tm_value(lo[i], hi[i]);
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int n = 0; n < L; ++n) s = fma(h[2 * M + j + n], a[n], s);
+    y[j] = M == 0 ? 0.5 * s : s;
+  }
+#pragma unroll
+  for (int i = 0; i < L; ++i) tm_st(tm + 2 * ((M + i) * (M + i) + ridx(M, PART)), y[i]);
+}
+template <int N>
+__device__ __forceinline__ void stage3_t(double* w, uint32_t tm, const double2* ca, const double2* cb) {
+  int lo[2 * N + 1], hi[2 * N + 1];
+  double x[2 * N + 1], t[2 * N + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) tm_ld(tm + 2 * (N * N + i), lo[i], hi[i]);
+  tm_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) x[i] = tm_value(lo[i], hi[i]);
+  apply_fixed<N, true, true, true>(x, t, 0);
+  zrot<N>(t, cb);
+  apply_fixed<N, true, false, false>(t, x, 0);
+  zrot<N>(x, ca);
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) w[N * N + i] = x[i];
+}
+template <int P, int N = 0>
+__device__ __forceinline__ void stage1_t_all(const double* w, uint32_t tm, double r, double rn, const double2* ca,
+                                             const double2* cb) {
+  stage1_t<N>(w, tm, rn, ca, cb);
+  order_fence();
+  if constexpr (N < P) stage1_t_all<P, N + 1>(w, tm, r, rn * r, ca, cb);
+}
+template <int P, int M = 0>
+__device__ __forceinline__ void stage2_t_all(uint32_t tm, const double* h) {
+  stage2_t<P, M, 0>(tm, h);
+  if constexpr (M > 0) stage2_t<P, M, 1>(tm, h);
+  if constexpr (M < P) stage2_t_all<P, M + 1>(tm, h);
+}
+template <int P, int N = 0>
+__device__ __forceinline__ void stage3_t_all(double* w, uint32_t tm, const double2* ca, const double2* cb) {
+  stage3_t<N>(w, tm, ca, cb);
+  order_fence();
+  if constexpr (N < P) stage3_t_all<P, N + 1>(w, tm, ca, cb);
+}
+template <int P>
+__device__ __noinline__ void pair_transform_tmem(double* w, double r, double2 e1, double2 e2, double iu) {
+  const uint32_t tm = tm_warp_base();
+  double2 ca[P + 1], cb[P + 1];
+  ca[0] = cb[0] = make_double2(1.0, 0.0);
+  ca[1] = e1;
+  cb[1] = e2;
+#pragma unroll
+  for (int m = 2; m <= P; ++m) {
+    ca[m] = make_double2(fma(ca[m - 1].x, e1.x, -ca[m - 1].y * e1.y), fma(ca[m - 1].x, e1.y, ca[m - 1].y * e1.x));
+    cb[m] = make_double2(fma(cb[m - 1].x, e2.x, -cb[m - 1].y * e2.y), fma(cb[m - 1].x, e2.y, cb[m - 1].y * e2.x));
+  }
+  stage1_t_all<P>(w, tm, r, 1.0, ca, cb);
+  tm_wait_st();
+  double h[2 * P + 1];  // Hankel entries k! / u^{k+1}
+  h[0] = iu;
+#pragma unroll
+  for (int k = 1; k <= 2 * P; ++k) h[k] = h[k - 1] * (k * iu);
+  stage2_t_all<P>(tm, h);
+  tm_wait_st();
+#if FMM_V4_STAGE_SYNC == 1 || FMM_V4_STAGE_SYNC == 3
+  stage_barrier();
+#endif
+  stage3_t_all<P>(w, tm, ca, cb);
+}
+
 #if FMM_V4_CIMM
 // one pair's rotation-translation-rotation, in place in the lane's row w. Not inlined: the fixed
 // operator's constant-bank entries are then DFMA operands at immediate addresses (no load
@@ -869,6 +992,19 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double* const wb = sm4 + (size_t)warp * 32 * NRS;
   double* const w = wb + lane * NRS;
+  // tensor memory: all 512 columns of the SM (one CTA per SM); warp k owns lanes 32 (k % 4) .. + 31 (the only
+  // ones it can address) and columns 256 (k / 4) .. + 2 NR - 1
+  if constexpr (use_tmem<P>) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&tm_base_s))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
   // static round-robin over equal-work units; every warp of the CTA runs the same number of
   // units and chunks (a barrier after each stage keeps the warps on the same instructions:
   // the unrolled code is larger than the instruction cache, so warps in step share its fetches)
@@ -1004,6 +1140,8 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
       __syncwarp();
       if constexpr (use_rep<P>)
         pair_transform_rep<P>(w, r, e1, e2, iu);
+      else if constexpr (use_tmem<P>)
+        pair_transform_tmem<P>(w, r, e1, e2, iu);
       else
         pair_transform<P>(w, r, e1, e2, iu);
 #else
@@ -1110,6 +1248,11 @@ __global__ void __launch_bounds__(32 * kMaxWarpsPerCta, 1) m2l_v4_kernel(const V
 #endif
     }
     if (cur >= 0) finish_segment<P>(a, u, cur, cur == tprev, cur == tnext, acc, lane);
+  }
+  if constexpr (use_tmem<P>) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm_base_s) : "memory");
   }
 }
 

@@ -813,7 +813,11 @@ __device__ __forceinline__ void pair_transform_rep(double* w, double r, double2 
 #ifndef FMM_V4_TMEM
 #define FMM_V4_TMEM 0  // the lane-private hand-offs stage 1 -> 2 -> 3 through tensor memory (32x32b tcgen05.st / ld:
                        // thread i <-> TMEM lane i, the row as 2 NR 32-bit columns) instead of shared memory:
-                       // 4 of the 8 passes over the row leave the shared-memory pipe (orders p <= 10, <= 8 warps)
+                       // 4 of the 8 passes over the row leave the shared-memory pipe (orders p <= 10, <= 8 warps).
+                       // 1: one double per access (x2); 2: degree blocks as x4..x32 pieces, stage 2's Re / Im as x4.
+                       // Parity green (127 GPU tests each); measured slower: configs[2] M2L 2.63 -> 2.73 (1) / 2.85 ms
+                       // (2), configs[3] 18.1 -> 18.7 / 18.1 ms: tensor-memory reads cost at least the shared-memory
+                       // wavefronts they replace (profiles/r2_m2l_bound.md); off.
 #endif
 template <int P>
 constexpr bool use_tmem = FMM_V4_TMEM != 0 && P <= 10 && !use_rep<P>;
@@ -840,6 +844,66 @@ __device__ __forceinline__ double tm_value(int lo, int hi) {
   return __hiloint2double(hi, lo);
 }
 
+// K consecutive 32-bit columns of the calling thread's TMEM lane (K a power of two)
+template <int K>
+__device__ __forceinline__ void tm_ldk(uint32_t addr, int* r);
+template <int K>
+__device__ __forceinline__ void tm_stk(uint32_t addr, const int* r);
+template <>
+__device__ __forceinline__ void tm_ldk<2>(uint32_t addr, int* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr) : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_stk<2>(uint32_t addr, const int* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(r[0]), "r"(r[1]) : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ldk<4>(uint32_t addr, int* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr) : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_stk<4>(uint32_t addr, const int* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ldk<8>(uint32_t addr, int* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]) : "r"(addr) : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_stk<8>(uint32_t addr, const int* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]) : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ldk<16>(uint32_t addr, int* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(addr) : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_stk<16>(uint32_t addr, const int* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ldk<32>(uint32_t addr, int* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(addr) : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_stk<32>(uint32_t addr, const int* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
+}
+
+constexpr int pow2_le(int c) { return c >= 32 ? 32 : c >= 16 ? 16 : c >= 8 ? 8 : c >= 4 ? 4 : 2; }
+// C columns (even) from / to column offset OFF of the block at addr, in power-of-two pieces
+template <int C, int OFF = 0>
+__device__ __forceinline__ void tm_ld_block(uint32_t addr, int* r) {
+  constexpr int K = pow2_le(C);
+  tm_ldk<K>(addr + OFF, r + OFF);
+  if constexpr (C > K) tm_ld_block<C - K, OFF + K>(addr, r);
+}
+template <int C, int OFF = 0>
+__device__ __forceinline__ void tm_st_block(uint32_t addr, const int* r) {
+  constexpr int K = pow2_le(C);
+  tm_stk<K>(addr + OFF, r + OFF);
+  if constexpr (C > K) tm_st_block<C - K, OFF + K>(addr, r);
+}
 template <int N>
 __device__ __forceinline__ void stage1_t(const double* w, uint32_t tm, double rn, const double2* ca, const double2* cb) {
   double x[2 * N + 1], t[2 * N + 1];
@@ -849,8 +913,18 @@ __device__ __forceinline__ void stage1_t(const double* w, uint32_t tm, double rn
   apply_fixed<N, false, true, false>(x, t, 0);
   zrot<N>(t, cb);
   apply_fixed<N, false, false, false>(t, x, 0);
+#if FMM_V4_TMEM >= 2
+  int rr[2 * (2 * N + 1)];
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) {
+    rr[2 * i] = __double2loint(x[i]);
+    rr[2 * i + 1] = __double2hiint(x[i]);
+  }
+  tm_st_block<2 * (2 * N + 1)>(tm + 2 * N * N, rr);
+#else
 #pragma unroll
   for (int i = 0; i < 2 * N + 1; ++i) tm_st(tm + 2 * (N * N + i), x[i]);
+#endif
 }
 template <int P, int M, int PART>
 __device__ __forceinline__ void stage2_t(uint32_t tm, const double* h) {
@@ -872,15 +946,52 @@ __device__ __forceinline__ void stage2_t(uint32_t tm, const double* h) {
 #pragma unroll
   for (int i = 0; i < L; ++i) tm_st(tm + 2 * ((M + i) * (M + i) + ridx(M, PART)), y[i]);
 }
+// stage 2 of order M >= 1, Re and Im together (adjacent in the row: one x4 access per degree)
+template <int P, int M>
+__device__ __forceinline__ void stage2_t4(uint32_t tm, const double* h) {
+  constexpr int L = P + 1 - M;
+  int rr[L][4];
+  double ar[L], ai[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) tm_ldk<4>(tm + 2 * ((M + i) * (M + i) + 2 * M - 1), rr[i]);
+  tm_wait_ld();
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    ar[i] = tm_value(rr[i][0], rr[i][1]);
+    ai[i] = tm_value(rr[i][2], rr[i][3]);
+  }
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    double sr = 0.0, si = 0.0;
+#pragma unroll
+    for (int n = 0; n < L; ++n) sr = fma(h[2 * M + j + n], ar[n], sr);
+#pragma unroll
+    for (int n = 0; n < L; ++n) si = fma(h[2 * M + j + n], ai[n], si);
+    rr[j][0] = __double2loint(sr);
+    rr[j][1] = __double2hiint(sr);
+    rr[j][2] = __double2loint(si);
+    rr[j][3] = __double2hiint(si);
+  }
+#pragma unroll
+  for (int i = 0; i < L; ++i) tm_stk<4>(tm + 2 * ((M + i) * (M + i) + 2 * M - 1), rr[i]);
+}
 template <int N>
 __device__ __forceinline__ void stage3_t(double* w, uint32_t tm, const double2* ca, const double2* cb) {
-  int lo[2 * N + 1], hi[2 * N + 1];
   double x[2 * N + 1], t[2 * N + 1];
+#if FMM_V4_TMEM >= 2
+  int rr[2 * (2 * N + 1)];
+  tm_ld_block<2 * (2 * N + 1)>(tm + 2 * N * N, rr);
+  tm_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 2 * N + 1; ++i) x[i] = tm_value(rr[2 * i], rr[2 * i + 1]);
+#else
+  int lo[2 * N + 1], hi[2 * N + 1];
 #pragma unroll
   for (int i = 0; i < 2 * N + 1; ++i) tm_ld(tm + 2 * (N * N + i), lo[i], hi[i]);
   tm_wait_ld();
 #pragma unroll
   for (int i = 0; i < 2 * N + 1; ++i) x[i] = tm_value(lo[i], hi[i]);
+#endif
   apply_fixed<N, true, true, true>(x, t, 0);
   zrot<N>(t, cb);
   apply_fixed<N, true, false, false>(t, x, 0);
@@ -897,8 +1008,15 @@ __device__ __forceinline__ void stage1_t_all(const double* w, uint32_t tm, doubl
 }
 template <int P, int M = 0>
 __device__ __forceinline__ void stage2_t_all(uint32_t tm, const double* h) {
+#if FMM_V4_TMEM >= 2
+  if constexpr (M == 0)
+    stage2_t<P, 0, 0>(tm, h);
+  else
+    stage2_t4<P, M>(tm, h);
+#else
   stage2_t<P, M, 0>(tm, h);
   if constexpr (M > 0) stage2_t<P, M, 1>(tm, h);
+#endif
   if constexpr (M < P) stage2_t_all<P, M + 1>(tm, h);
 }
 template <int P, int N = 0>
@@ -1309,12 +1427,13 @@ void size_v4(fmm_plan_s& P_, int64_t npairs) {
   using G = V4Geo<P>;
   M2L4& V = P_.m2l4;
   const size_t sh = (size_t)32 * G::NRS * sizeof(double);
-  FMM_CUDA(cudaFuncSetAttribute(m2l_v4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   int nsm = 148;
   FMM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P_.device));
   cudaFuncAttributes fa;
   FMM_CUDA(cudaFuncGetAttributes(&fa, m2l_v4_kernel<P>));
-  const int by_smem = (int)((227 * 1024) / sh), by_regs = 65536 / (32 * std::max(1, fa.numRegs));
+  const size_t dyn_max = (size_t)227 * 1024 - fa.sharedSizeBytes;  // (static: the tensor-memory base, if used)
+  FMM_CUDA(cudaFuncSetAttribute(m2l_v4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
+  const int by_smem = (int)(dyn_max / sh), by_regs = 65536 / (32 * std::max(1, fa.numRegs));
   const int fit = std::max(1, std::min({by_smem, by_regs, kMaxWarpsPerCta}));
   V.wpc = std::max(1, std::min(V.warps_per_sm > 0 ? V.warps_per_sm : fit, fit));
   V.smem = sh * V.wpc;

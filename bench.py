@@ -441,10 +441,11 @@ def main():
     else:
         dom, dflops, dms = "near (P2P+L2P)", near_flops, near_ms
     achieved = dflops / (dms * 1e-3) / 1e12
-    traffic = None
+    traffic = None  # the ncu capture is of the default workload (configs[2]); other configs report null
     try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(dom, {}).get("bytes")
+        if args.config == "c3":
+            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get(dom, {}).get("bytes")
     except (OSError, ValueError):
         pass
     p2p_m2l_tflops = (m2l_flops + near_flops) / ((m2l_ms + near_ms) * 1e-3) / 1e12

@@ -273,7 +273,8 @@ def test_full_size_sampled_parity(torch_cuda, name, k):
                                                   ("sphere", 20000, 5, 40, 0.35), ("cube", 20000, 14, 64, 0.4),
                                                   ("plummer", 20000, 9, 40, 0.5), ("sphere", 20000, 12, 128, 0.4),
                                                   ("cube", 20000, 2, 32, 0.5), ("sphere", 20000, 3, 40, 0.4),
-                                                  ("plummer", 20000, 4, 16, 0.5), ("cube", 8000, 0, 16, 0.5)])
+                                                  ("plummer", 20000, 4, 16, 0.5), ("cube", 8000, 0, 16, 0.5),
+                                                  ("plummer", 20000, 11, 40, 0.5)])
 def test_m2l_variants(torch_cuda, monkeypatch, variant, dist, n, p, ncrit, theta):
     """The four M2L formulations — v1 matrix-free O(p^4) per pair (the paper's analytic end),
     v2 precomputed dense translation-invariant operators on DMMA, v3 the

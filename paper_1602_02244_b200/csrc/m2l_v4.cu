@@ -665,7 +665,7 @@ struct V4Geo {
 #ifndef FMM_V4_REP_MINP
 #define FMM_V4_REP_MINP 11  // orders from this one up use the shared-body form: at p = 12 the pair function is 140 KB and
                             // the kernel waits on instructions (no_instruction 2.9 warps per issue, FP64 pipe 24 %):
-                            // configs[4] M2L 227 -> 216 ms
+                            // configs[4] M2L 227 -> 216 ms (202 ms with the passes per degree group)
 #endif
 template <int P>
 constexpr bool use_rep = FMM_V4_REP != 0 || P >= FMM_V4_REP_MINP;
@@ -798,17 +798,67 @@ __device__ __noinline__ void pass2(double* w, double r, double iu) {
   for (int n = 1; n <= P; ++n) rp[n] = rp[n - 1] * r;
   stage2r_all<P>(w, h, rp);
 }
+#ifndef FMM_V4_REP_GROUPS
+#define FMM_V4_REP_GROUPS 1  // the two passes of a stage taken per group of degrees (a stage acts on each degree alone):
+                             // a group's code (<= ~14 KB) is still in the 32 KB L1.5 instruction cache for its second
+                             // call, where a whole-stage pass (34 KB at p = 12) has evicted itself (configs[4] M2L
+                             // 216.1 -> 202.0 ms)
+#endif
+template <int P, int N0, int N1, int N = N0>
+__device__ __forceinline__ void body1_range(double* w, const double2* cs) {
+  body1<N>(w, cs);
+  order_fence();
+  if constexpr (N < N1) body1_range<P, N0, N1, N + 1>(w, cs);
+}
+template <int P, int N0, int N1, int N = N0>
+__device__ __forceinline__ void body3_range(double* w, const double2* cs) {
+  body3<N>(w, cs);
+  order_fence();
+  if constexpr (N < N1) body3_range<P, N0, N1, N + 1>(w, cs);
+}
+template <int P, int N0, int N1>
+__device__ __noinline__ void pass1g(double* w, double2 e) {
+  double2 cs[N1 + 1];
+  phasors<N1>(cs, e);
+  body1_range<P, N0, N1>(w, cs);
+}
+template <int P, int N0, int N1>
+__device__ __noinline__ void pass3g(double* w, double2 e) {
+  double2 cs[N1 + 1];
+  phasors<N1>(cs, e);
+  body3_range<P, N0, N1>(w, cs);
+}
 template <int P>
 __device__ __forceinline__ void pair_transform_rep(double* w, double r, double2 e1, double2 e2, double iu) {
   const double2 ea = make_double2(-e1.x, -e1.y), eb = make_double2(-e2.x, -e2.y);  // angles a + pi, b + pi
-  pass1<P>(w, ea);
-  pass1<P>(w, eb);
+  constexpr bool grouped = FMM_V4_REP_GROUPS != 0 && P >= 8;
+  constexpr int G1 = P - 4, G2 = P - 2;  // degree groups [0, G1], (G1, G2], (G2, P]: about equal code
+  if constexpr (grouped) {
+    pass1g<P, 0, G1>(w, ea);
+    pass1g<P, 0, G1>(w, eb);
+    pass1g<P, G1 + 1, G2>(w, ea);
+    pass1g<P, G1 + 1, G2>(w, eb);
+    pass1g<P, G2 + 1, P>(w, ea);
+    pass1g<P, G2 + 1, P>(w, eb);
+  } else {
+    pass1<P>(w, ea);
+    pass1<P>(w, eb);
+  }
   pass2<P>(w, r, iu);
 #if FMM_V4_STAGE_SYNC == 1 || FMM_V4_STAGE_SYNC == 3
   stage_barrier();
 #endif
-  pass3<P>(w, eb);
-  pass3<P>(w, ea);
+  if constexpr (grouped) {
+    pass3g<P, 0, G1>(w, eb);
+    pass3g<P, 0, G1>(w, ea);
+    pass3g<P, G1 + 1, G2>(w, eb);
+    pass3g<P, G1 + 1, G2>(w, ea);
+    pass3g<P, G2 + 1, P>(w, eb);
+    pass3g<P, G2 + 1, P>(w, ea);
+  } else {
+    pass3<P>(w, eb);
+    pass3<P>(w, ea);
+  }
 }
 #ifndef FMM_V4_TMEM
 #define FMM_V4_TMEM 0  // the lane-private hand-offs stage 1 -> 2 -> 3 through tensor memory (32x32b tcgen05.st / ld:

@@ -798,6 +798,56 @@ __device__ __noinline__ void pass2(double* w, double r, double iu) {
   for (int n = 1; n <= P; ++n) rp[n] = rp[n - 1] * r;
   stage2r_all<P>(w, h, rp);
 }
+#ifndef FMM_V4_REP_S2SPLIT
+#define FMM_V4_REP_S2SPLIT 1  // stage 2 of the orders m >= 1 as one function called for the Re and then the Im parts (the
+                              // same Hankel products one coefficient further along the row; the conjugation K as the
+                              // sign of r^n): its code is fetched once (configs[4] M2L 201.9 -> 190.4 ms)
+#endif
+// stage 2 of order M >= 1 for one part: wp = w + part (the part's coefficient of degree n sits at n^2 + 2M - 1 + part)
+template <int P, int M>
+__device__ __forceinline__ void stage2p(double* wp, const double* h, const double* rp) {
+  constexpr int L = P + 1 - M;
+  double a[L], y[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) a[i] = wp[(M + i) * (M + i) + 2 * M - 1] * rp[M + i];
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    double t = 0.0;
+#pragma unroll
+    for (int n = 0; n < L; ++n) t = fma(h[2 * M + j + n], a[n], t);
+    y[j] = t;
+  }
+#pragma unroll
+  for (int i = 0; i < L; ++i) wp[(M + i) * (M + i) + 2 * M - 1] = y[i];
+}
+template <int P, int M = 1>
+__device__ __forceinline__ void stage2p_all(double* wp, const double* h, const double* rp) {
+  stage2p<P, M>(wp, h, rp);
+  order_fence();
+  if constexpr (M < P) stage2p_all<P, M + 1>(wp, h, rp);
+}
+template <int P>
+__device__ __noinline__ void pass2g(double* wp, double r, double iu, double sgn) {
+  double h[2 * P + 1], rp[P + 1];  // Hankel entries k! / u^{k+1}; sgn r^n
+  h[0] = iu;
+#pragma unroll
+  for (int k = 1; k <= 2 * P; ++k) h[k] = h[k - 1] * (k * iu);
+  rp[0] = sgn;
+#pragma unroll
+  for (int n = 1; n <= P; ++n) rp[n] = rp[n - 1] * r;
+  stage2p_all<P>(wp, h, rp);
+}
+template <int P>
+__device__ __noinline__ void pass2m0(double* w, double r, double iu) {
+  double h[2 * P + 1], rp[P + 1];
+  h[0] = iu;
+#pragma unroll
+  for (int k = 1; k <= 2 * P; ++k) h[k] = h[k - 1] * (k * iu);
+  rp[0] = 1.0;
+#pragma unroll
+  for (int n = 1; n <= P; ++n) rp[n] = rp[n - 1] * r;
+  stage2r<P, 0, 0>(w, h, rp);
+}
 #ifndef FMM_V4_REP_GROUPS
 #define FMM_V4_REP_GROUPS 1  // the two passes of a stage taken per group of degrees (a stage acts on each degree alone):
                              // a group's code (<= ~14 KB) is still in the 32 KB L1.5 instruction cache for its second
@@ -844,7 +894,13 @@ __device__ __forceinline__ void pair_transform_rep(double* w, double r, double2 
     pass1<P>(w, ea);
     pass1<P>(w, eb);
   }
+#if FMM_V4_REP_S2SPLIT
+  pass2m0<P>(w, r, iu);
+  pass2g<P>(w, r, iu, 1.0);
+  pass2g<P>(w + 1, r, iu, -1.0);
+#else
   pass2<P>(w, r, iu);
+#endif
 #if FMM_V4_STAGE_SYNC == 1 || FMM_V4_STAGE_SYNC == 3
   stage_barrier();
 #endif
